@@ -1,0 +1,205 @@
+/*
+ * sgm.h — C ABI of the B200 sGraph-candidate backend (libsgm.so).
+ *
+ * The backend executes *instantiated sGraph candidates* (a block graph with a
+ * concrete mapping and concrete grid / for-loop sizes) on one B200 (sm_100a),
+ * times them, and runs finite-field equivalence checks on device.  It is the
+ * drop-in replacement for the reference's CPU interpreter:
+ *
+ *   reference interface                          replaced by
+ *   ------------------------------------------   ------------------------------------
+ *   symfuse.interp.run_concrete                  sgm_plan_create + sgm_plan_run
+ *     (pkg/src/symfuse/interp.py:128-212)          (+ sgm_plan_run_host for host buffers)
+ *   symfuse.interp.run_program                   sgm_plan_create(program-as-plan) + run
+ *     (interp.py:69-83)
+ *   symfuse.tuner.score_interp                   sgm_plan_time
+ *     (pkg/src/symfuse/tuner.py:160-174)
+ *   symfuse.interp.random_equiv_test             sgm_ff_fill + sgm_plan_run (SGM_FF) +
+ *     (interp.py:238-286)                          sgm_compare_u32 / sgm_rel_err
+ *   errors.py exception classes                  sgm_status codes + sgm_last_error()
+ *     (pkg/src/symfuse/errors.py:1-38)
+ *
+ * Everything is plain C: POD descriptors, raw device pointers, sizes and an
+ * opaque stream handle (a CUstream / cudaStream_t, or NULL for the legacy
+ * stream).  No torch types cross this boundary.
+ *
+ * Conventions
+ *  - Every entry point returns an sgm_status; on failure a thread-local message
+ *    is available from sgm_last_error().
+ *  - Tensors are dense row-major.  Input slot k of a plan reads program input k
+ *    (program order, symfuse `Program.inputs`); output slot k writes program
+ *    output k (`Program.outputs`).  Element type follows the plan's number
+ *    system: SGM_F64 double, SGM_F32 float, SGM_BF16 bfloat16 (uint16 bits),
+ *    SGM_FF uint32 residues modulo 2^31-1.
+ *  - Threading: one host thread drives one device; plan handles are not
+ *    thread-safe, sgm_plan_create may be called concurrently (compilation is
+ *    independent per plan).
+ */
+#ifndef SGM_H_
+#define SGM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGM_ABI_VERSION 1
+
+#define SGM_MAX_RANK 4
+#define SGM_MAX_GRID 3
+#define SGM_MAX_NODES 64
+#define SGM_MAX_SLOTS 16
+
+/* Status codes.  1..6 map onto the reference's errors.py classes. */
+typedef enum {
+  SGM_OK = 0,
+  SGM_ERR_SHAPE = 1,          /* ShapeError           (errors.py:5)  */
+  SGM_ERR_DIVISIBILITY = 2,   /* DivisibilityError    (errors.py:9)  */
+  SGM_ERR_WRITE_CONFLICT = 3, /* WriteConflictError   (errors.py:33) */
+  SGM_ERR_UNSUPPORTED = 4,    /* UnsupportedOpError   (errors.py:25) */
+  SGM_ERR_CONSTRAINT = 5,     /* ConstraintError      (errors.py:17) */
+  SGM_ERR_INVALID = 6,        /* malformed descriptor / numpy-style ValueError */
+  SGM_ERR_CUDA = 100,         /* CUDA driver failure */
+  SGM_ERR_NVRTC = 101,        /* kernel compilation failure */
+  SGM_ERR_RESOURCE = 102,     /* smem / cluster / memory limits */
+  SGM_ERR_NOT_INIT = 103
+} sgm_status;
+
+/* Number systems a plan computes in. */
+typedef enum {
+  SGM_F64 = 0,  /* fp64 storage + compute (the reference's dtype)            */
+  SGM_F32 = 1,  /* fp32 storage + compute                                    */
+  SGM_BF16 = 2, /* bf16 storage, fp32 compute                                */
+  SGM_FF = 3    /* uint32 residues mod p = 2^31-1; exp/silu/sqrt keyed hashes */
+} sgm_numsys;
+
+/* Block-graph node kinds (symfuse graph.py:49-65). */
+typedef enum {
+  SGM_INPUT = 0, SGM_OUTPUT = 1, SGM_MATMUL = 2, SGM_EXP = 3, SGM_SILU = 4,
+  SGM_SQUARE = 5, SGM_SQRT = 6, SGM_DIV = 7, SGM_MUL = 8, SGM_ADD = 9,
+  SGM_SUM = 10, SGM_ACCUM = 11, SGM_SCALE = 12
+} sgm_kind;
+
+/* One program tensor seen through a loader (input slot) or saver (output slot). */
+typedef struct {
+  int32_t rank;
+  int32_t _pad;
+  int64_t dims[SGM_MAX_RANK];
+} sgm_slot_desc;
+
+/* One block-graph node.  Mirrors symfuse BlockNode (graph.py:190-208) plus the
+ * concrete tile shape of ConcreteGraph.shapes (graph.py:406-441) and, for
+ * loaders / savers, the partition of each data dim:
+ *   grid_mask[d] bit g set  <=> mapping[MapVar(tensor, d, grid[g])] == 1
+ *   loop_split[d] != 0      <=> mapping[MapVar(tensor, d, loop)] == 1 (loaders only)
+ * Splits nest in grid order, then the loop (interp.py:90-113). */
+typedef struct {
+  int32_t kind;            /* sgm_kind */
+  int32_t n_inputs;
+  int32_t inputs[2];
+  int32_t slot;            /* loader: input slot; saver: output slot; else -1 */
+  int32_t axis;            /* sum axis (left-indexed data dim), else -1 */
+  int64_t const_num;       /* scale factor numerator / denominator */
+  int64_t const_den;
+  int32_t rank;
+  int32_t _pad;
+  int64_t shape[SGM_MAX_RANK];       /* concrete per-block tile shape */
+  uint32_t grid_mask[SGM_MAX_RANK];
+  int32_t loop_split[SGM_MAX_RANK];
+} sgm_node_desc;
+
+/* Planner hints (0 = automatic). */
+typedef struct {
+  int32_t max_cluster;     /* cap on CTAs per logical block sharing a cluster (1..16) */
+  int32_t target_ctas;     /* desired total CTAs (default 2 x SMs) */
+  int32_t threads;         /* threads per CTA (default 256) */
+  int32_t smem_budget;     /* bytes of dynamic smem per CTA the planner may use */
+  int32_t no_loop_split;   /* 1: run the for-loop sequentially inside every CTA */
+  int32_t no_hoist;        /* 1: do not hoist loop-invariant body nodes */
+  int32_t use_tcgen05;     /* -1 off, 0 auto, 1 force where legal */
+  int32_t _reserved[9];
+} sgm_plan_hints;
+
+typedef struct {
+  int32_t abi_version;     /* must be SGM_ABI_VERSION */
+  int32_t numsys;          /* sgm_numsys */
+  int32_t n_inputs;
+  int32_t n_outputs;
+  sgm_slot_desc inputs[SGM_MAX_SLOTS];
+  sgm_slot_desc outputs[SGM_MAX_SLOTS];
+  int32_t n_nodes;
+  int32_t n_grid;          /* number of grid dims (1..3) */
+  int64_t grid[SGM_MAX_GRID]; /* concrete grid sizes (params[x], params[y], params[z]) */
+  int64_t n_loop;          /* params[i] */
+  sgm_node_desc nodes[SGM_MAX_NODES];
+  sgm_plan_hints hints;
+} sgm_plan_desc;
+
+/* What the planner decided (for reports, tests and the profiler). */
+typedef struct {
+  int64_t logical_blocks;  /* prod(grid) */
+  int64_t ctas;            /* launched CTAs */
+  int32_t cluster;         /* CTAs per cluster */
+  int32_t threads;
+  int32_t smem_bytes;      /* dynamic smem per CTA */
+  int32_t loop_parts;      /* loop iterations spread over this many CTAs */
+  int64_t free_parts;      /* independent CTAs per logical block */
+  int64_t scratch_bytes;   /* global scratch for tiles that do not fit smem */
+  double compile_ms;       /* 0 on a cache hit */
+  int32_t cache_hit;
+  int32_t n_tcgen05;       /* matmul nodes realised with tcgen05 */
+  uint64_t source_hash;
+  char kernel_name[64];
+  char plan_summary[448];
+} sgm_plan_info;
+
+typedef struct sgm_plan sgm_plan;
+
+int sgm_abi_version(void);
+const char* sgm_last_error(void);
+
+/* Bind the calling thread to `device` (primary context) and load the driver. */
+int sgm_init(int device);
+/* Directory for the persistent cubin cache (NULL = default next to libsgm.so). */
+int sgm_set_cache_dir(const char* path);
+
+/* Validate + plan + generate + compile (or cache-hit) a candidate kernel. */
+int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out);
+int sgm_plan_info_get(const sgm_plan* plan, sgm_plan_info* info);
+/* Copy the generated CUDA source (NUL-terminated, truncated to cap). Returns length via *len. */
+int sgm_plan_source(const sgm_plan* plan, char* buf, size_t cap, size_t* len);
+int sgm_plan_destroy(sgm_plan* plan);
+
+/* Outputs are first filled with NaN (fp) / 0xFFFFFFFF (FF) when init_outputs != 0,
+ * reproducing the reference's NaN-initialised outputs (interp.py:147-152). */
+int sgm_plan_run(sgm_plan* plan, const void* const* inputs, void* const* outputs,
+                 int init_outputs, void* stream);
+/* Host-buffer variant: H2D of inputs, run, D2H of outputs, all on `stream`
+ * (pinned staging owned by the plan).  This is the e2e path. */
+int sgm_plan_run_host(sgm_plan* plan, const void* const* host_inputs,
+                      void* const* host_outputs, void* stream);
+/* Time `iters` back-to-back launches (after `warmup`) with CUDA events on
+ * `stream`.  If `rot` > 1, `inputs` holds rot*n_inputs pointers (rotating input
+ * sets, so successive launches miss L2).  Writes mean microseconds per launch. */
+int sgm_plan_time(sgm_plan* plan, const void* const* inputs, void* const* outputs,
+                  int rot, int warmup, int iters, void* stream, double* mean_us);
+
+/* Counter-based uniform residues in [0, p): value(i) = mix64(key + i*G) mod p with
+ * key = mix64(seed ^ mix64(salt)).  Same function as oracle/ff_np.py:ff_uniform. */
+int sgm_ff_fill(uint32_t* dst, int64_t n, uint64_t seed, uint64_t salt, void* stream);
+/* Number of positions where a != b (uint32). */
+int sgm_compare_u32(const uint32_t* a, const uint32_t* b, int64_t n, void* stream,
+                    int64_t* mismatches);
+/* rel_err(a, b) = max|a-b| / (1 + max|b|), +inf if a is non-finite (interp.py:228-231).
+ * numsys selects the element type of both buffers (F64/F32/BF16). */
+int sgm_rel_err(const void* a, const void* b, int64_t n, int numsys, void* stream,
+                double* out);
+/* Fill with a standard-normal-like deterministic pattern (for timing inputs). */
+int sgm_fill_normal(void* dst, int64_t n, int numsys, uint64_t seed, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGM_H_ */

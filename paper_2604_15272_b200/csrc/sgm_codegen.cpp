@@ -1,0 +1,1222 @@
+// sgm_codegen.cpp — planner + CUDA code generator for instantiated sGraph candidates.
+//
+// Input: an sgm_plan_desc (the POD lowering of a symfuse ConcreteGraph).
+// Output: CUDA C++ source of ONE kernel that executes every logical block of the
+// candidate, for NVRTC (sm_100a).
+//
+// Execution model (B200-first):
+//  * A logical block (one grid coordinate, interp.py:156-158) is executed by
+//    FREE x CLUSTER CTAs.  Free parts split an axis class that no node reduces
+//    (independent CTAs, no communication); cluster parts split a reduced axis
+//    class or the for-loop iterations (interp.py:162) and combine partial tiles
+//    through DSMEM (cluster all-reduce), so the IR's "no inter-block reduction"
+//    rule (graph.py:311-320) is kept while a logical block can still use many SMs.
+//  * Tiles are materialised in shared memory (dense rank-4, compute type) with
+//    liveness-based reuse; loader tiles consumed only as the large operand of a
+//    matmul stay *views* of HBM and are streamed once (ld.global.nc, 16-byte
+//    vectors, unrolled for memory-level parallelism).
+//  * Loop-invariant body nodes are hoisted; accumulators are zeroed once and
+//    summed per iteration (interp.py:171-176); the epilogue runs after the loop
+//    with loop-split loaders on their last tile (interp.py:182-189).
+//  * Savers write each output cell from exactly one CTA; write conflicts are
+//    detected statically with the reference's outcome (interp.py:200-203).
+
+#include "sgm_codegen.h"
+
+#include <algorithm>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <set>
+#include <sstream>
+
+namespace sgmcg {
+
+typedef int64_t i64;
+typedef uint32_t u32;
+
+uint64_t fnv1a(const std::string& s, uint64_t h) {
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+static const uint32_t kP = 0x7FFFFFFFu;
+static uint32_t ffmul(uint32_t a, uint32_t b) { return (uint32_t)(((uint64_t)a * b) % kP); }
+static uint32_t ffpow(uint32_t a, uint32_t e) {
+  uint32_t r = 1;
+  while (e) {
+    if (e & 1) r = ffmul(r, a);
+    a = ffmul(a, a);
+    e >>= 1;
+  }
+  return r;
+}
+uint32_t ff_const(int64_t num, int64_t den) {
+  int64_t n = num % (int64_t)kP;
+  if (n < 0) n += kP;
+  int64_t d = den % (int64_t)kP;
+  if (d < 0) d += kP;
+  return ffmul((uint32_t)n, ffpow((uint32_t)d, kP - 2));
+}
+
+namespace {
+
+enum Store { ST_NONE = 0, ST_VIEW, ST_SMEM, ST_GLOBAL };
+
+struct Node {
+  int kind = 0, nin = 0, in[2] = {-1, -1}, slot = -1, axis = -1;
+  i64 cnum = 0, cden = 1;
+  int rank = 0;
+  i64 sh[4] = {1, 1, 1, 1};   // full per-block tile (rank-4, left padded)
+  i64 sl[4] = {1, 1, 1, 1};   // per-CTA slice
+  u32 gmask[4] = {0, 0, 0, 0};
+  int lsplit[4] = {0, 0, 0, 0};
+  int cls[4] = {-1, -1, -1, -1};
+  bool body = false, hoist = false, loopdep = false;
+  int store = ST_NONE;
+  int off = 0;                 // smem offset or scratch offset
+  std::vector<int> cons;
+  u32 pend = 0;                // pending cluster bits (partial over these CTAs)
+  bool deferred = false;
+  // matmul realisation
+  bool gemv = false;
+  int vn = 1, ks = 1, unr = 4;
+  bool shfl = false;
+  i64 red_bytes = 0;
+  int red_off = 0;
+};
+
+struct Class {
+  i64 extent = 1;
+  bool reduced = false;
+  bool twice = false;
+  int parts = 1;
+  bool cluster = false;  // split across the cluster (reduced) or free CTAs
+  int bit_shift = 0;     // cluster rank bit field
+  i64 radix = 1;         // free-part mixed radix
+};
+
+struct Ev {
+  enum { NODE, FLUSH, LOOP_BEGIN, LOOP_END } type;
+  int node = -1;
+  std::vector<int> flush;
+};
+
+struct Interval {
+  int id;       // node id, or -(1+k) for transient k
+  int start, end;
+  i64 bytes;
+};
+
+struct Gen {
+  const sgm_plan_desc& d;
+  int num_sms;
+  GenResult R;
+  int ns = 0;      // number system
+  int es = 4;      // storage element size
+  int ec = 4;      // compute element size
+  int ea = 4;      // accumulator element size
+  int vecw = 4;    // elements per 16-byte vector (storage)
+  int NT = 256;
+  std::vector<Node> nodes;
+  std::vector<Class> cls;
+  i64 grid[3] = {1, 1, 1};
+  int ngrid = 1;
+  i64 nloop = 1;
+  i64 LB = 1;
+  int LP = 1;            // loop parts
+  int loop_shift = 0;
+  int CL = 1;            // cluster size
+  i64 FP = 1;            // free parts
+  bool loop_split_ok = false;
+  i64 in_strides[SGM_MAX_SLOTS][4];
+  i64 in_dims[SGM_MAX_SLOTS][4];
+  i64 out_strides[SGM_MAX_SLOTS][4];
+  i64 out_dims[SGM_MAX_SLOTS][4];
+  int in_rank[SGM_MAX_SLOTS];
+  int out_rank[SGM_MAX_SLOTS];
+  std::vector<Ev> sched;
+  int loop_begin_pos = -1, loop_end_pos = -1;
+  std::vector<i64> flush_tmp_bytes;   // per schedule position
+  std::map<std::pair<int, int>, int> flush_tmp_off;  // (pos,node) -> smem offset
+  int smem_peak = 0;
+  i64 scratch_per_cta = 0;
+  int budget = 200 * 1024;
+
+  Gen(const sgm_plan_desc& desc, int sms) : d(desc), num_sms(sms) {}
+
+  bool fail(int st, const std::string& msg) {
+    if (R.status == SGM_OK) {
+      R.status = st;
+      R.error = msg;
+    }
+    return false;
+  }
+
+  // ------------------------------------------------------------------ setup
+  bool load() {
+    if (d.abi_version != SGM_ABI_VERSION) return fail(SGM_ERR_INVALID, "abi version mismatch");
+    ns = d.numsys;
+    switch (ns) {
+      case SGM_F64: es = 8; ec = 8; ea = 8; break;
+      case SGM_F32: es = 4; ec = 4; ea = 4; break;
+      case SGM_BF16: es = 2; ec = 4; ea = 4; break;
+      case SGM_FF: es = 4; ec = 4; ea = 8; break;
+      default: return fail(SGM_ERR_INVALID, "unknown number system");
+    }
+    vecw = 16 / es;
+    NT = d.hints.threads > 0 ? d.hints.threads : 256;
+    if (NT % 32 || NT > 1024) return fail(SGM_ERR_INVALID, "threads must be a multiple of 32 <= 1024");
+    if (d.hints.smem_budget > 0) budget = d.hints.smem_budget;
+    if (d.n_grid < 1 || d.n_grid > 3) return fail(SGM_ERR_INVALID, "n_grid must be 1..3");
+    ngrid = d.n_grid;
+    for (int g = 0; g < ngrid; ++g) {
+      if (d.grid[g] < 1) return fail(SGM_ERR_DIVISIBILITY, "grid size must be positive");
+      grid[g] = d.grid[g];
+      LB *= grid[g];
+    }
+    if (d.n_loop < 1) return fail(SGM_ERR_DIVISIBILITY, "loop size must be positive");
+    nloop = d.n_loop;
+    if (d.n_inputs < 0 || d.n_inputs > SGM_MAX_SLOTS || d.n_outputs < 0 || d.n_outputs > SGM_MAX_SLOTS)
+      return fail(SGM_ERR_INVALID, "bad slot count");
+    auto slot_setup = [&](const sgm_slot_desc& s, i64* dims, i64* strides, int& rank) -> bool {
+      if (s.rank < 1 || s.rank > 4) return fail(SGM_ERR_INVALID, "slot rank must be 1..4");
+      rank = s.rank;
+      int pad = 4 - s.rank;
+      for (int k = 0; k < 4; ++k) dims[k] = 1;
+      for (int k = 0; k < s.rank; ++k) {
+        if (s.dims[k] < 1) return fail(SGM_ERR_INVALID, "slot dims must be positive");
+        dims[pad + k] = s.dims[k];
+      }
+      i64 st = 1;
+      for (int k = 3; k >= 0; --k) {
+        strides[k] = st;
+        st *= dims[k];
+      }
+      return true;
+    };
+    for (int k = 0; k < d.n_inputs; ++k)
+      if (!slot_setup(d.inputs[k], in_dims[k], in_strides[k], in_rank[k])) return false;
+    for (int k = 0; k < d.n_outputs; ++k)
+      if (!slot_setup(d.outputs[k], out_dims[k], out_strides[k], out_rank[k])) return false;
+    if (d.n_nodes < 1 || d.n_nodes > SGM_MAX_NODES) return fail(SGM_ERR_INVALID, "bad node count");
+    nodes.resize(d.n_nodes);
+    for (int n = 0; n < d.n_nodes; ++n) {
+      const sgm_node_desc& s = d.nodes[n];
+      Node& x = nodes[n];
+      x.kind = s.kind;
+      x.nin = s.n_inputs;
+      if (x.nin < 0 || x.nin > 2) return fail(SGM_ERR_INVALID, "bad input count");
+      for (int k = 0; k < x.nin; ++k) {
+        x.in[k] = s.inputs[k];
+        if (x.in[k] < 0 || x.in[k] >= n) return fail(SGM_ERR_SHAPE, "forward edge in block graph");
+        nodes[x.in[k]].cons.push_back(n);
+      }
+      x.slot = s.slot;
+      x.axis = s.axis;
+      x.cnum = s.const_num;
+      x.cden = s.const_den;
+      int want = 0;
+      switch (x.kind) {
+        case SGM_INPUT: want = 0; break;
+        case SGM_OUTPUT: case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT:
+        case SGM_SUM: case SGM_ACCUM: case SGM_SCALE: want = 1; break;
+        case SGM_MATMUL: case SGM_DIV: case SGM_MUL: case SGM_ADD: want = 2; break;
+        default: return fail(SGM_ERR_UNSUPPORTED, "unknown op kind");
+      }
+      if (x.nin != want) return fail(SGM_ERR_INVALID, "wrong number of inputs for op");
+      if (x.kind == SGM_INPUT && (x.slot < 0 || x.slot >= d.n_inputs)) return fail(SGM_ERR_INVALID, "bad input slot");
+      if (x.kind == SGM_OUTPUT && (x.slot < 0 || x.slot >= d.n_outputs)) return fail(SGM_ERR_INVALID, "bad output slot");
+      if (x.kind == SGM_SCALE && x.cden == 0) return fail(SGM_ERR_INVALID, "scale with zero denominator");
+      for (int k = 0; k < 4; ++k) {
+        x.gmask[k] = 0;
+        x.lsplit[k] = 0;
+      }
+      if (x.kind == SGM_INPUT || x.kind == SGM_OUTPUT) {
+        int r = x.kind == SGM_INPUT ? in_rank[x.slot] : out_rank[x.slot];
+        int pad = 4 - r;
+        for (int k = 0; k < r; ++k) {
+          x.gmask[pad + k] = s.grid_mask[k] & ((1u << ngrid) - 1u);
+          x.lsplit[pad + k] = (x.kind == SGM_INPUT) ? (s.loop_split[k] != 0) : 0;
+        }
+      }
+    }
+    return true;
+  }
+
+  // Tile shapes from the mapping, as the reference slices (interp.py:90-125);
+  // op shapes with numpy semantics (interp.py:45-66).
+  bool shapes() {
+    char buf[256];
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& x = nodes[n];
+      if (x.kind == SGM_INPUT) {
+        x.rank = in_rank[x.slot];
+        for (int k = 0; k < 4; ++k) {
+          i64 w = in_dims[x.slot][k];
+          if (w > 1) {
+            for (int g = 0; g < ngrid; ++g)
+              if (x.gmask[k] >> g & 1u) {
+                if (w % grid[g]) {
+                  snprintf(buf, sizeof buf, "extent %" PRId64 " not divisible by %" PRId64, w, grid[g]);
+                  return fail(SGM_ERR_SHAPE, buf);
+                }
+                w /= grid[g];
+              }
+            if (x.lsplit[k]) {
+              if (w % nloop) {
+                snprintf(buf, sizeof buf, "extent %" PRId64 " not divisible by %" PRId64, w, nloop);
+                return fail(SGM_ERR_SHAPE, buf);
+              }
+              w /= nloop;
+            }
+          } else {
+            x.gmask[k] = 0;
+            x.lsplit[k] = 0;
+          }
+          x.sh[k] = w;
+        }
+        continue;
+      }
+      const Node& a = nodes[x.in[0]];
+      switch (x.kind) {
+        case SGM_OUTPUT: case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT:
+        case SGM_ACCUM: case SGM_SCALE:
+          x.rank = a.rank;
+          for (int k = 0; k < 4; ++k) x.sh[k] = a.sh[k];
+          break;
+        case SGM_SUM: {
+          x.rank = a.rank;
+          if (x.axis < 0 || x.axis >= a.rank) return fail(SGM_ERR_INVALID, "axis out of bounds for sum");
+          int ax = x.axis + 4 - a.rank;
+          for (int k = 0; k < 4; ++k) x.sh[k] = (k == ax) ? 1 : a.sh[k];
+          break;
+        }
+        case SGM_DIV: case SGM_MUL: case SGM_ADD: {
+          const Node& b = nodes[x.in[1]];
+          x.rank = std::max(a.rank, b.rank);
+          for (int k = 0; k < 4; ++k) {
+            if (a.sh[k] == b.sh[k] || b.sh[k] == 1) x.sh[k] = a.sh[k];
+            else if (a.sh[k] == 1) x.sh[k] = b.sh[k];
+            else return fail(SGM_ERR_INVALID, "operands could not be broadcast together");
+          }
+          break;
+        }
+        case SGM_MATMUL: {
+          const Node& b = nodes[x.in[1]];
+          if (a.rank < 2 || b.rank < 2) return fail(SGM_ERR_INVALID, "matmul operands need rank >= 2");
+          if (a.sh[3] != b.sh[2]) return fail(SGM_ERR_INVALID, "matmul: mismatch in its core dimension");
+          x.rank = std::max(a.rank, b.rank);
+          for (int k = 0; k < 2; ++k) {
+            if (a.sh[k] == b.sh[k] || b.sh[k] == 1) x.sh[k] = a.sh[k];
+            else if (a.sh[k] == 1) x.sh[k] = b.sh[k];
+            else return fail(SGM_ERR_INVALID, "matmul: batch dims could not be broadcast");
+          }
+          x.sh[2] = a.sh[2];
+          x.sh[3] = b.sh[3];
+          break;
+        }
+        default: return fail(SGM_ERR_UNSUPPORTED, "unknown op");
+      }
+    }
+    // Saver regions must match their tiles (interp.py:196-199).
+    for (auto& x : nodes) {
+      if (x.kind != SGM_OUTPUT) continue;
+      i64 reg[4];
+      for (int k = 0; k < 4; ++k) {
+        i64 w = out_dims[x.slot][k];
+        if (w > 1) {
+          for (int g = 0; g < ngrid; ++g)
+            if (x.gmask[k] >> g & 1u) {
+              if (w % grid[g]) return fail(SGM_ERR_SHAPE, "saver region not divisible");
+              w /= grid[g];
+            }
+        } else {
+          x.gmask[k] = 0;
+        }
+        reg[k] = w;
+      }
+      bool same = (x.rank == out_rank[x.slot]);
+      for (int k = 0; k < 4; ++k) same = same && reg[k] == x.sh[k];
+      if (!same) {
+        std::ostringstream os;
+        os << "saver slot " << x.slot << ": tile (";
+        for (int k = 4 - x.rank; k < 4; ++k) os << x.sh[k] << (k < 3 ? "," : "");
+        os << ") vs region (";
+        for (int k = 4 - out_rank[x.slot]; k < 4; ++k) os << reg[k] << (k < 3 ? "," : "");
+        os << ")";
+        return fail(SGM_ERR_SHAPE, os.str());
+      }
+    }
+    // Static write-conflict detection: two logical blocks write the same cell iff
+    // some grid dim with size > 1 is absent from the saver's output map, or two
+    // savers target one output (interp.py:200-203 raises on the second write).
+    std::vector<int> writers(d.n_outputs, 0);
+    for (auto& x : nodes) {
+      if (x.kind != SGM_OUTPUT) continue;
+      writers[x.slot]++;
+      for (int g = 0; g < ngrid; ++g) {
+        if (grid[g] <= 1) continue;
+        bool used = false;
+        for (int k = 0; k < 4; ++k) used = used || (x.gmask[k] >> g & 1u);
+        if (!used) return fail(SGM_ERR_WRITE_CONFLICT, "output slot " + std::to_string(x.slot) +
+                                                        ": blocks overwrite cells (grid dim " +
+                                                        std::to_string(g) + " not in output map)");
+      }
+    }
+    for (int s = 0; s < d.n_outputs; ++s) {
+      if (writers[s] > 1 && LB >= 1)
+        return fail(SGM_ERR_WRITE_CONFLICT, "output slot " + std::to_string(s) + " written by two savers");
+    }
+    return true;
+  }
+
+  // ------------------------------------------------------------ structure
+  void structure() {
+    // body = accumulators and their ancestors (graph.py:242-254)
+    for (int n = (int)nodes.size() - 1; n >= 0; --n) {
+      Node& x = nodes[n];
+      if (x.kind == SGM_ACCUM) x.body = true;
+      if (x.body)
+        for (int k = 0; k < x.nin; ++k) nodes[x.in[k]].body = true;
+    }
+    for (auto& x : nodes) {
+      bool dep = false;
+      if (x.kind == SGM_INPUT)
+        for (int k = 0; k < 4; ++k) dep = dep || x.lsplit[k];
+      if (x.kind == SGM_ACCUM) dep = true;
+      for (int k = 0; k < x.nin; ++k) dep = dep || nodes[x.in[k]].loopdep;
+      x.loopdep = dep;
+      x.hoist = x.body && !dep && !d.hints.no_hoist;
+    }
+    // loop split legality
+    bool any_accum = false;
+    for (auto& x : nodes) any_accum = any_accum || x.kind == SGM_ACCUM;
+    loop_split_ok = nloop > 1 && any_accum && !d.hints.no_loop_split;
+    for (auto& x : nodes) {
+      for (int k = 0; k < x.nin; ++k) {
+        const Node& p = nodes[x.in[k]];
+        if (x.body && !x.hoist && p.kind == SGM_ACCUM && x.kind != SGM_ACCUM) loop_split_ok = false;
+        if (x.body && p.kind == SGM_ACCUM) loop_split_ok = false;  // running totals consumed in-loop
+        if (!x.body && p.body && !p.hoist && p.kind != SGM_ACCUM) loop_split_ok = false;
+      }
+    }
+    // axis classes
+    int N = (int)nodes.size();
+    std::vector<int> par(N * 4);
+    for (int i = 0; i < N * 4; ++i) par[i] = i;
+    std::function<int(int)> find = [&](int v) { return par[v] == v ? v : par[v] = find(par[v]); };
+    auto unite = [&](int a, int b) {
+      a = find(a);
+      b = find(b);
+      if (a != b) par[a] = b;
+    };
+    auto id = [](int n, int k) { return n * 4 + k; };
+    for (int n = 0; n < N; ++n) {
+      Node& x = nodes[n];
+      if (x.kind == SGM_INPUT) continue;
+      if (x.kind == SGM_MATMUL) {
+        const Node& a = nodes[x.in[0]];
+        const Node& b = nodes[x.in[1]];
+        for (int k = 0; k < 2; ++k) {
+          if (x.sh[k] > 1 && a.sh[k] == x.sh[k]) unite(id(n, k), id(x.in[0], k));
+          if (x.sh[k] > 1 && b.sh[k] == x.sh[k]) unite(id(n, k), id(x.in[1], k));
+        }
+        if (x.sh[2] > 1) unite(id(n, 2), id(x.in[0], 2));
+        if (x.sh[3] > 1) unite(id(n, 3), id(x.in[1], 3));
+        if (a.sh[3] > 1) unite(id(x.in[0], 3), id(x.in[1], 2));
+      } else if (x.kind == SGM_SUM) {
+        int ax = x.axis + 4 - nodes[x.in[0]].rank;
+        for (int k = 0; k < 4; ++k)
+          if (k != ax && x.sh[k] > 1) unite(id(n, k), id(x.in[0], k));
+      } else {
+        for (int j = 0; j < x.nin; ++j) {
+          const Node& a = nodes[x.in[j]];
+          for (int k = 0; k < 4; ++k)
+            if (x.sh[k] > 1 && a.sh[k] == x.sh[k]) unite(id(n, k), id(x.in[j], k));
+        }
+      }
+    }
+    std::map<int, int> root2cls;
+    for (int n = 0; n < N; ++n)
+      for (int k = 0; k < 4; ++k) {
+        if (nodes[n].sh[k] <= 1) continue;
+        int r = find(id(n, k));
+        auto it = root2cls.find(r);
+        int c;
+        if (it == root2cls.end()) {
+          c = (int)cls.size();
+          root2cls[r] = c;
+          Class C;
+          C.extent = nodes[n].sh[k];
+          cls.push_back(C);
+        } else {
+          c = it->second;
+        }
+        nodes[n].cls[k] = c;
+        if (cls[c].extent != nodes[n].sh[k]) cls[c].twice = true;  // inconsistent: never split
+      }
+    for (int n = 0; n < N; ++n) {
+      Node& x = nodes[n];
+      for (int k = 0; k < 4; ++k)
+        for (int j = k + 1; j < 4; ++j)
+          if (x.cls[k] >= 0 && x.cls[k] == x.cls[j]) cls[x.cls[k]].twice = true;
+      if (x.kind == SGM_MATMUL) {
+        int c = nodes[x.in[0]].cls[3];
+        if (c >= 0) cls[c].reduced = true;
+      }
+      if (x.kind == SGM_SUM) {
+        int c = nodes[x.in[0]].cls[x.axis + 4 - nodes[x.in[0]].rank];
+        if (c >= 0) cls[c].reduced = true;
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ planning
+  static i64 prod4(const i64* s) { return s[0] * s[1] * s[2] * s[3]; }
+
+  i64 loader_traffic(const Node& x) const {
+    i64 b = prod4(x.sh) * es;
+    if (x.body && x.loopdep) b *= nloop;
+    return b;
+  }
+  bool has_cls(const Node& x, int c) const {
+    for (int k = 0; k < 4; ++k)
+      if (x.cls[k] == c) return true;
+    return false;
+  }
+  bool loader_loop_split(const Node& x) const {
+    for (int k = 0; k < 4; ++k)
+      if (x.lsplit[k]) return true;
+    return false;
+  }
+
+  void decide_views() {
+    for (auto& x : nodes) {
+      if (x.kind == SGM_OUTPUT) { x.store = ST_NONE; continue; }
+      x.store = ST_SMEM;
+    }
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& x = nodes[n];
+      if (x.kind != SGM_INPUT || x.cons.empty()) continue;
+      bool view = true;
+      for (int c : x.cons) {
+        const Node& m = nodes[c];
+        if (m.kind != SGM_MATMUL) { view = false; break; }
+        int other = m.in[0] == n ? m.in[1] : m.in[0];
+        if (m.in[0] == n && m.in[1] == n) { view = false; break; }
+        const Node& o = nodes[other];
+        // stream the larger operand; the smaller one is reused from smem
+        if (prod4(x.sh) < prod4(o.sh) || (prod4(x.sh) == prod4(o.sh) && m.in[1] != n)) { view = false; break; }
+      }
+      if (view) x.store = ST_VIEW;
+    }
+  }
+
+  void slices() {
+    for (auto& x : nodes)
+      for (int k = 0; k < 4; ++k) {
+        int c = x.cls[k];
+        x.sl[k] = (c >= 0) ? x.sh[k] / cls[c].parts : x.sh[k];
+      }
+  }
+
+  void split_plan() {
+    int max_cluster = d.hints.max_cluster > 0 ? std::min(16, d.hints.max_cluster) : 8;
+    i64 target = d.hints.target_ctas > 0 ? d.hints.target_ctas : 2LL * num_sms;
+    i64 W = 0;
+    for (auto& x : nodes)
+      if (x.kind == SGM_INPUT) W += loader_traffic(x);
+    const i64 kMinBytesPerCta = 32 * 1024;
+    i64 max_parts = std::max<i64>(1, W / kMinBytesPerCta);
+    auto cost_of = [&](int c) -> i64 {
+      i64 cost = 0;
+      for (auto& x : nodes)
+        if (x.kind == SGM_INPUT && !has_cls(x, c)) cost += loader_traffic(x);
+      return cost;
+    };
+    auto loop_cost = [&]() -> i64 {
+      i64 cost = 0;
+      for (auto& x : nodes)
+        if (x.kind == SGM_INPUT && !loader_loop_split(x)) cost += loader_traffic(x);
+      return cost;
+    };
+    for (int iter = 0; iter < 64; ++iter) {
+      i64 tot = FP * CL;
+      if (LB * tot >= target || tot * 2 > max_parts) break;
+      int best = -1;
+      bool best_cluster = false;
+      i64 best_cost = 0, best_rem = 0;
+      for (int c = 0; c < (int)cls.size(); ++c) {
+        Class& C = cls[c];
+        if (C.twice) continue;
+        if (C.extent % (C.parts * 2)) continue;
+        bool isc = C.reduced;
+        if (isc && CL * 2 > max_cluster) continue;
+        i64 cost = cost_of(c);
+        i64 rem = C.extent / C.parts;
+        bool better = best == -1 || cost < best_cost || (cost == best_cost && !isc && best_cluster) ||
+                      (cost == best_cost && isc == best_cluster && rem > best_rem);
+        if (better) { best = c; best_cost = cost; best_cluster = isc; best_rem = rem; }
+      }
+      if (loop_split_ok && nloop % (LP * 2) == 0 && CL * 2 <= max_cluster) {
+        i64 cost = loop_cost();
+        i64 rem = nloop / LP;
+        bool better = best == -1 || cost < best_cost || (cost == best_cost && best_cluster && rem > best_rem);
+        if (better) { best = -2; best_cost = cost; best_cluster = true; best_rem = rem; }
+      }
+      if (best == -1) break;
+      if (best_cost * 4 > W && LB * tot * 2 > num_sms) break;  // >25% redundant traffic: not worth it
+      if (best == -2) { LP *= 2; CL *= 2; }
+      else {
+        cls[best].parts *= 2;
+        if (cls[best].reduced) { cls[best].cluster = true; CL *= 2; }
+        else FP *= 2;
+      }
+    }
+    finalize_layout();
+  }
+
+  void finalize_layout() {
+    // cluster rank bit fields: loop first, then reduced classes
+    int shift = 0;
+    loop_shift = 0;
+    if (LP > 1) { loop_shift = 0; while ((1 << shift) < LP) ++shift; }
+    i64 radix = 1;
+    for (auto& C : cls) {
+      if (C.parts <= 1) continue;
+      if (C.cluster) {
+        C.bit_shift = shift;
+        int b = 0;
+        while ((1 << b) < C.parts) ++b;
+        shift += b;
+      } else {
+        C.radix = radix;
+        radix *= C.parts;
+      }
+    }
+    FP = radix;
+    CL = 1 << shift;
+  }
+
+  u32 class_bits(int c) const {
+    const Class& C = cls[c];
+    if (!C.cluster || C.parts <= 1) return 0;
+    return (u32)(C.parts - 1) << C.bit_shift;
+  }
+  u32 loop_bits() const { return LP > 1 ? (u32)(LP - 1) << loop_shift : 0; }
+
+  // pending partials + schedule
+  void schedule() {
+    for (auto& x : nodes) { x.pend = 0; x.deferred = false; }
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& x = nodes[n];
+      if (x.kind == SGM_MATMUL) {
+        int c = nodes[x.in[0]].cls[3];
+        if (c >= 0) x.pend |= class_bits(c);
+      } else if (x.kind == SGM_SUM) {
+        int c = nodes[x.in[0]].cls[x.axis + 4 - nodes[x.in[0]].rank];
+        if (c >= 0) x.pend |= class_bits(c);
+      }
+    }
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& x = nodes[n];
+      if (x.pend && x.body && !x.cons.empty()) {
+        bool all_acc = true;
+        for (int c : x.cons) all_acc = all_acc && nodes[c].kind == SGM_ACCUM;
+        x.deferred = all_acc;
+      }
+      if (x.kind == SGM_ACCUM) {
+        const Node& p = nodes[x.in[0]];
+        x.pend = (p.deferred ? p.pend : 0) | loop_bits();
+      }
+    }
+    sched.clear();
+    std::set<int> pending;
+    auto flush_for = [&](const Node& x, bool force_all) {
+      std::vector<int> fl;
+      bool need = force_all;
+      for (int k = 0; k < x.nin && !need; ++k) {
+        int p = x.in[k];
+        if (pending.count(p) && !(x.kind == SGM_ACCUM && nodes[p].deferred)) need = true;
+      }
+      if (!need) return;
+      for (int p : pending)
+        if (!nodes[p].deferred || nodes[p].kind == SGM_ACCUM) fl.push_back(p);
+      if (fl.empty()) return;
+      for (int p : fl) pending.erase(p);
+      Ev e;
+      e.type = Ev::FLUSH;
+      e.flush = fl;
+      sched.push_back(e);
+    };
+    auto push_node = [&](int n) {
+      Node& x = nodes[n];
+      flush_for(x, false);
+      Ev e;
+      e.type = Ev::NODE;
+      e.node = n;
+      sched.push_back(e);
+      if (x.pend) pending.insert(n);
+    };
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (nodes[n].hoist) push_node(n);
+    bool has_loop = false;
+    for (auto& x : nodes) has_loop = has_loop || (x.body && !x.hoist);
+    if (has_loop) {
+      // hoisted partials must be complete before the loop re-reads them
+      {
+        std::vector<int> fl;
+        for (int p : pending)
+          if (!nodes[p].deferred) fl.push_back(p);
+        if (!fl.empty()) {
+          for (int p : fl) pending.erase(p);
+          Ev e;
+          e.type = Ev::FLUSH;
+          e.flush = fl;
+          sched.push_back(e);
+        }
+      }
+      Ev b;
+      b.type = Ev::LOOP_BEGIN;
+      loop_begin_pos = (int)sched.size();
+      sched.push_back(b);
+      for (int n = 0; n < (int)nodes.size(); ++n)
+        if (nodes[n].body && !nodes[n].hoist) push_node(n);
+      Ev en;
+      en.type = Ev::LOOP_END;
+      loop_end_pos = (int)sched.size();
+      sched.push_back(en);
+    } else {
+      loop_begin_pos = loop_end_pos = -1;
+    }
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (!nodes[n].body) push_node(n);
+  }
+
+  // matmul realisation choices (depend on slices)
+  void matmul_choices() {
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& x = nodes[n];
+      if (x.kind != SGM_MATMUL) continue;
+      const Node& a = nodes[x.in[0]];
+      const Node& b = nodes[x.in[1]];
+      x.gemv = false;
+      x.red_bytes = 0;
+      i64 M = x.sl[2], K = a.sl[3], NN = x.sl[3];
+      if (b.store == ST_VIEW && a.store != ST_VIEW && M <= 16 && NN >= 1) {
+        // B stride along n must be 1 (row-major view), alignment for vectors
+        int accw = ea / 4;  // 32-bit registers per accumulator
+        int vn = 1;
+        for (int cand : {16 / es, 8 / es, 4 / es, 2 / es, 1}) {
+          if (cand < 1) continue;
+          if (NN % cand) continue;
+          if (M * cand * accw > 64 && cand > 1) continue;
+          bool ok = true;
+          const i64* st = in_strides[b.slot];
+          for (int k = 0; k < 3; ++k)
+            if (in_dims[b.slot][k] > 1 && st[k] % cand) ok = false;
+          // all offset coefficients along dim 3 are multiples of the slice width
+          if (b.sl[3] % cand) ok = false;
+          if (!ok) continue;
+          vn = cand;
+          break;
+        }
+        x.gemv = true;
+        x.vn = vn;
+        i64 NV = NN / vn;
+        i64 items = x.sl[0] * x.sl[1] * NV;
+        i64 ks = 1;
+        while (items * ks * 2 <= NT && ks * 2 <= K) ks *= 2;
+        x.ks = (int)ks;
+        i64 per_thread = (K + ks - 1) / ks;
+        x.unr = per_thread >= 8 ? 8 : (per_thread >= 4 ? 4 : (per_thread >= 2 ? 2 : 1));
+        bool nv_pow2 = (NV & (NV - 1)) == 0;
+        i64 work = items * ks;
+        x.shfl = nv_pow2 && ((work % NT == 0) || (work < NT && work % 32 == 0));
+        i64 kin = (!x.shfl || NV >= 32) ? 1 : std::min<i64>(32 / NV, ks);
+        i64 kout = ks / kin;
+        if (kout > 1) x.red_bytes = kout * items * M * vn * ea;
+      }
+    }
+  }
+
+  // liveness-based smem allocation; returns peak bytes
+  int allocate() {
+    int S = (int)sched.size();
+    std::vector<int> pos_of(nodes.size(), -1);
+    for (int p = 0; p < S; ++p)
+      if (sched[p].type == Ev::NODE) pos_of[sched[p].node] = p;
+    std::vector<Interval> iv;
+    std::vector<int> last(nodes.size(), -1);
+    for (int p = 0; p < S; ++p) {
+      const Ev& e = sched[p];
+      if (e.type == Ev::NODE) {
+        const Node& x = nodes[e.node];
+        for (int k = 0; k < x.nin; ++k) last[x.in[k]] = std::max(last[x.in[k]], p);
+      } else if (e.type == Ev::FLUSH) {
+        for (int f : e.flush) last[f] = std::max(last[f], p);
+      }
+    }
+    int tcount = 0;
+    flush_tmp_off.clear();
+    std::vector<std::pair<std::pair<int, int>, int>> flush_ids;
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& x = nodes[n];
+      if (x.store != ST_SMEM || x.kind == SGM_OUTPUT) continue;
+      int st = pos_of[n];
+      if (x.kind == SGM_ACCUM) st = loop_begin_pos;
+      int en = std::max(last[n], pos_of[n]);
+      if (loop_begin_pos >= 0 && st < loop_begin_pos && en > loop_begin_pos) en = std::max(en, loop_end_pos);
+      if (x.kind == SGM_ACCUM) en = std::max(en, loop_end_pos);
+      Interval I;
+      I.id = n;
+      I.start = st;
+      I.end = en;
+      I.bytes = prod4(x.sl) * ec;
+      iv.push_back(I);
+    }
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (nodes[n].kind == SGM_MATMUL && nodes[n].red_bytes > 0) {
+        Interval I;
+        I.id = -(1 + tcount++);
+        I.start = I.end = pos_of[n];
+        I.bytes = nodes[n].red_bytes;
+        iv.push_back(I);
+      }
+    for (int p = 0; p < S; ++p)
+      if (sched[p].type == Ev::FLUSH)
+        for (int f : sched[p].flush) {
+          Interval I;
+          I.id = -(1 + tcount++);
+          I.start = I.end = p;
+          I.bytes = prod4(nodes[f].sl) * ec;
+          iv.push_back(I);
+          flush_ids.push_back({{p, f}, I.id});
+        }
+    std::sort(iv.begin(), iv.end(), [](const Interval& a, const Interval& b) {
+      if (a.start != b.start) return a.start < b.start;
+      return a.bytes > b.bytes;
+    });
+    std::vector<std::pair<Interval, i64>> placed;
+    i64 peak = 0;
+    std::map<int, i64> off_of;
+    for (auto& I : iv) {
+      std::vector<std::pair<i64, i64>> busy;
+      for (auto& pl : placed)
+        if (!(pl.first.end < I.start || pl.first.start > I.end)) busy.push_back({pl.second, pl.second + pl.first.bytes});
+      std::sort(busy.begin(), busy.end());
+      i64 off = 0;
+      for (auto& b : busy) {
+        if (off + I.bytes <= b.first) break;
+        off = std::max(off, (b.second + 15) / 16 * 16);
+      }
+      placed.push_back({I, off});
+      off_of[I.id] = off;
+      peak = std::max(peak, off + I.bytes);
+    }
+    for (auto& x : nodes) x.off = 0;
+    for (auto& kv : off_of)
+      if (kv.first >= 0) nodes[kv.first].off = (int)kv.second;
+    int t = 0;
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (nodes[n].kind == SGM_MATMUL && nodes[n].red_bytes > 0) nodes[n].red_off = (int)off_of[-(1 + t++)];
+    for (auto& fi : flush_ids) flush_tmp_off[fi.first] = (int)off_of[fi.second];
+    // global scratch for tiles that did not fit
+    scratch_per_cta = 0;
+    for (auto& x : nodes)
+      if (x.store == ST_GLOBAL) {
+        x.off = (int)scratch_per_cta;
+        scratch_per_cta += (prod4(x.sl) * ec + 255) / 256 * 256;
+      }
+    return (int)peak;
+  }
+
+  bool fit() {
+    // grow splits on the largest tile while over budget, then spill to global
+    for (int iter = 0; iter < 64; ++iter) {
+      slices();
+      schedule();
+      matmul_choices();
+      smem_peak = allocate();
+      if (smem_peak <= budget) return true;
+      // largest smem tile
+      int big = -1;
+      i64 bb = 0;
+      for (int n = 0; n < (int)nodes.size(); ++n) {
+        const Node& x = nodes[n];
+        if (x.store != ST_SMEM || x.kind == SGM_OUTPUT) continue;
+        i64 b = prod4(x.sl) * ec;
+        if (b > bb) { bb = b; big = n; }
+      }
+      if (big < 0) break;
+      // try a split of one of its classes (more CTAs share the tile)
+      int max_cluster = d.hints.max_cluster > 0 ? std::min(16, d.hints.max_cluster) : 8;
+      int bestc = -1;
+      i64 bestrem = 0;
+      for (int k = 0; k < 4; ++k) {
+        int c = nodes[big].cls[k];
+        if (c < 0 || cls[c].twice) continue;
+        if (cls[c].extent % (cls[c].parts * 2)) continue;
+        if (cls[c].reduced && CL * 2 > max_cluster) continue;
+        i64 rem = cls[c].extent / cls[c].parts;
+        if (rem > bestrem) { bestrem = rem; bestc = c; }
+      }
+      if (bestc >= 0 && bestrem >= 2) {
+        cls[bestc].parts *= 2;
+        if (cls[bestc].reduced) cls[bestc].cluster = true;
+        finalize_layout();
+        continue;
+      }
+      // spill the largest tile that never takes part in a DSMEM reduction
+      int sp = -1;
+      i64 sb = 0;
+      for (int n = 0; n < (int)nodes.size(); ++n) {
+        const Node& x = nodes[n];
+        if (x.store != ST_SMEM || x.kind == SGM_OUTPUT || x.pend || x.kind == SGM_ACCUM) continue;
+        i64 b = prod4(x.sl) * ec;
+        if (b > sb) { sb = b; sp = n; }
+      }
+      if (sp < 0) break;
+      nodes[sp].store = ST_GLOBAL;
+    }
+    return smem_peak <= budget;
+  }
+
+  // ------------------------------------------------------------ emission
+  std::ostringstream os;
+
+  std::string tile_ptr(int n) const { return "t" + std::to_string(n); }
+
+  const char* nstruct() const {
+    switch (ns) {
+      case SGM_F64: return "sgm::NF64";
+      case SGM_F32: return "sgm::NF32";
+      case SGM_BF16: return "sgm::NBF16";
+      default: return "sgm::NFF";
+    }
+  }
+
+  std::string part_var(int c) const { return "p" + std::to_string(c); }
+
+  // global element offset of a loader/saver tile slice (interp.py:90-125 nesting)
+  std::string offset_expr(const Node& x, bool loader, const std::string& jexpr) const {
+    const i64* dims = loader ? in_dims[x.slot] : out_dims[x.slot];
+    const i64* st = loader ? in_strides[x.slot] : out_strides[x.slot];
+    std::ostringstream e;
+    e << "0LL";
+    static const char* gv[3] = {"gx", "gy", "gz"};
+    for (int k = 0; k < 4; ++k) {
+      i64 w = dims[k];
+      if (w <= 1) continue;
+      std::ostringstream dim;
+      bool any = false;
+      for (int g = 0; g < ngrid; ++g)
+        if (x.gmask[k] >> g & 1u) {
+          w /= grid[g];
+          dim << (any ? " + " : "") << gv[g] << " * " << w << "LL";
+          any = true;
+        }
+      if (loader && x.lsplit[k]) {
+        w /= nloop;
+        dim << (any ? " + " : "") << "(long long)(" << jexpr << ") * " << w << "LL";
+        any = true;
+      }
+      int c = x.cls[k];
+      if (c >= 0 && cls[c].parts > 1) {
+        dim << (any ? " + " : "") << part_var(c) << " * " << (x.sh[k] / cls[c].parts) << "LL";
+        any = true;
+      }
+      if (any) e << " + (" << dim.str() << ") * " << st[k] << "LL";
+    }
+    return e.str();
+  }
+
+  int io_vec(const Node& x, bool loader) const {
+    const i64* dims = loader ? in_dims[x.slot] : out_dims[x.slot];
+    const i64* st = loader ? in_strides[x.slot] : out_strides[x.slot];
+    int v = vecw;
+    if (x.sl[3] % v) return 1;
+    for (int k = 0; k < 3; ++k)
+      if (dims[k] > 1 && st[k] % v) return 1;
+    return v;
+  }
+
+  std::string const_literal(const Node& x) const {
+    char buf[64];
+    if (ns == SGM_FF) {
+      snprintf(buf, sizeof buf, "%uu", ff_const(x.cnum, x.cden));
+    } else if (ns == SGM_F64) {
+      double v = (double)x.cnum / (double)x.cden;
+      snprintf(buf, sizeof buf, "%a", v);
+    } else {
+      double v = (double)x.cnum / (double)x.cden;
+      snprintf(buf, sizeof buf, "%af", (double)(float)v);
+    }
+    return buf;
+  }
+
+  // dense strides of a slice with broadcast zeros where the consumer needs it
+  void dense_strides(const i64* sl, i64* out) const {
+    i64 s = 1;
+    for (int k = 3; k >= 0; --k) {
+      out[k] = sl[k] > 1 ? s : 0;
+      s *= sl[k];
+    }
+  }
+
+  std::string saver_pred(const Node& x) const {
+    std::ostringstream p;
+    p << "true";
+    const Node& src = nodes[x.in[0]];
+    for (int c = 0; c < (int)cls.size(); ++c) {
+      if (cls[c].parts <= 1) continue;
+      if (has_cls(src, c)) continue;
+      p << " && " << part_var(c) << " == 0";
+    }
+    if (LP > 1) p << " && jp == 0";
+    return p.str();
+  }
+
+  void emit_flush(const std::vector<int>& fl, int pos) {
+    os << "    sgm::cluster_sync();\n";
+    for (int f : fl) {
+      const Node& x = nodes[f];
+      u32 keep = (u32)(CL - 1) & ~x.pend;
+      os << "    sgm::cl_reduce<N, " << prod4(x.sl) << ", " << CL << ", " << keep << "u, NT>(" << tile_ptr(f)
+         << ", (C*)(sm + " << flush_tmp_off.at({pos, f}) << "), crank);\n";
+    }
+    os << "    sgm::cluster_sync();\n";
+    for (int f : fl) {
+      const Node& x = nodes[f];
+      os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) " << tile_ptr(f) << "[e] = ((const C*)(sm + "
+         << flush_tmp_off.at({pos, f}) << "))[e];\n";
+    }
+    os << "    __syncthreads();\n";
+  }
+
+  void emit_node(int n, bool in_loop) {
+    Node& x = nodes[n];
+    std::string J = in_loop ? "j" : std::to_string(nloop - 1);
+    os << "    // node " << n << " kind " << x.kind << " slice [" << x.sl[0] << "," << x.sl[1] << "," << x.sl[2] << ","
+       << x.sl[3] << "]\n";
+    switch (x.kind) {
+      case SGM_INPUT: {
+        if (x.store == ST_VIEW) return;  // streamed by its consumer (pointer built there)
+        std::string off = offset_expr(x, true, J);
+        const i64* st = in_strides[x.slot];
+        os << "    sgm::load_tile<N, " << x.sl[0] << ", " << x.sl[1] << ", " << x.sl[2] << ", " << x.sl[3] << ", "
+           << st[0] << "LL, " << st[1] << "LL, " << st[2] << "LL, " << st[3] << "LL, " << io_vec(x, true)
+           << ", NT>(" << tile_ptr(n) << ", (const S*)a.in[" << x.slot << "] + (" << off << "));\n";
+        break;
+      }
+      case SGM_OUTPUT: {
+        const Node& src = nodes[x.in[0]];
+        std::string off = offset_expr(x, false, "0");
+        const i64* st = out_strides[x.slot];
+        os << "    if (" << saver_pred(x) << ") sgm::store_tile<N, " << src.sl[0] << ", " << src.sl[1] << ", "
+           << src.sl[2] << ", " << src.sl[3] << ", " << st[0] << "LL, " << st[1] << "LL, " << st[2] << "LL, "
+           << st[3] << "LL, " << io_vec(src, false) << ", NT>((S*)a.out[" << x.slot << "] + (" << off << "), "
+           << tile_ptr(x.in[0]) << ");\n";
+        return;  // no barrier needed after a global store
+      }
+      case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT: case SGM_SCALE: {
+        const char* fn = x.kind == SGM_EXP ? "N::ex" : x.kind == SGM_SILU ? "N::silu" : x.kind == SGM_SQUARE ? "N::sq" : "N::sqr";
+        os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) " << tile_ptr(n) << "[e] = ";
+        if (x.kind == SGM_SCALE) os << "N::scale(" << tile_ptr(x.in[0]) << "[e], (C)" << const_literal(x) << ");\n";
+        else os << fn << "(" << tile_ptr(x.in[0]) << "[e]);\n";
+        break;
+      }
+      case SGM_ACCUM: {
+        os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) " << tile_ptr(n) << "[e] = N::add("
+           << tile_ptr(n) << "[e], " << tile_ptr(x.in[0]) << "[e]);\n";
+        break;
+      }
+      case SGM_DIV: case SGM_MUL: case SGM_ADD: {
+        const char* fn = x.kind == SGM_DIV ? "N::div" : x.kind == SGM_MUL ? "N::mul" : "N::add";
+        const Node& a = nodes[x.in[0]];
+        const Node& b = nodes[x.in[1]];
+        i64 sa[4], sb[4];
+        dense_strides(a.sl, sa);
+        dense_strides(b.sl, sb);
+        os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) {\n";
+        os << "      int r = e; const int i3 = r % " << x.sl[3] << "; r /= " << x.sl[3] << "; const int i2 = r % "
+           << x.sl[2] << "; r /= " << x.sl[2] << "; const int i1 = r % " << x.sl[1] << "; const int i0 = r / "
+           << x.sl[1] << ";\n";
+        auto idx = [&](const i64* s, const i64* sl) {
+          std::ostringstream q;
+          q << "0";
+          const char* iv[4] = {"i0", "i1", "i2", "i3"};
+          for (int k = 0; k < 4; ++k)
+            if (sl[k] > 1) q << " + " << iv[k] << " * " << s[k];
+          return q.str();
+        };
+        os << "      " << tile_ptr(n) << "[e] = " << fn << "(" << tile_ptr(x.in[0]) << "[" << idx(sa, a.sl) << "], "
+           << tile_ptr(x.in[1]) << "[" << idx(sb, b.sl) << "]);\n    }\n";
+        break;
+      }
+      case SGM_SUM: {
+        const Node& a = nodes[x.in[0]];
+        int ax = x.axis + 4 - a.rank;
+        os << "    sgm::sum_axis<N, " << a.sl[0] << ", " << a.sl[1] << ", " << a.sl[2] << ", " << a.sl[3] << ", " << ax
+           << ", NT>(" << tile_ptr(n) << ", " << tile_ptr(x.in[0]) << ");\n";
+        break;
+      }
+      case SGM_MATMUL: {
+        const Node& a = nodes[x.in[0]];
+        const Node& b = nodes[x.in[1]];
+        i64 M = x.sl[2], K = a.sl[3], NN = x.sl[3];
+        auto strides_of = [&](const Node& t, i64* s) {
+          if (t.store == ST_VIEW) {
+            const i64* st = in_strides[t.slot];
+            for (int k = 0; k < 4; ++k) s[k] = t.sl[k] > 1 ? st[k] : 0;
+          } else {
+            dense_strides(t.sl, s);
+          }
+        };
+        i64 sa[4], sb[4];
+        strides_of(a, sa);
+        strides_of(b, sb);
+        auto view_ptr = [&](const Node& t) {
+          return "((const S*)a.in[" + std::to_string(t.slot) + "] + (" + offset_expr(t, true, J) + "))";
+        };
+        std::string pa = a.store == ST_VIEW ? view_ptr(a) : tile_ptr(x.in[0]);
+        std::string pb = b.store == ST_VIEW ? view_ptr(b) : tile_ptr(x.in[1]);
+        if (x.gemv) {
+          os << "    sgm::mm_gemv<N, S, " << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
+             << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << sb[0] << "LL, " << sb[1]
+             << "LL, " << sb[2] << "LL, " << x.vn << ", " << x.ks << ", " << x.unr << ", "
+             << (x.shfl ? "true" : "false") << ", NT>(" << tile_ptr(n) << ", " << pa << ", " << pb << ", (A*)(sm + "
+             << x.red_off << "));\n";
+        } else {
+          std::string ta = a.store == ST_VIEW ? "S" : "C";
+          std::string tb = b.store == ST_VIEW ? "S" : "C";
+          os << "    sgm::mm_generic<N, " << ta << ", " << tb << ", " << x.sl[0] << ", " << x.sl[1] << ", " << M << ", "
+             << K << ", " << NN << ", " << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, "
+             << sb[0] << "LL, " << sb[1] << "LL, " << sb[2] << "LL, " << sb[3] << "LL, NT>(" << tile_ptr(n) << ", "
+             << pa << ", " << pb << ");\n";
+        }
+        break;
+      }
+      default: break;
+    }
+    os << "    __syncthreads();\n";
+  }
+
+  void emit() {
+    os << "#include \"sgm_dev.cuh\"\n";
+    os << "// generated by sgm_codegen.cpp: logical blocks " << LB << ", free parts " << FP << ", cluster " << CL
+       << ", loop parts " << LP << "\n";
+    os << "typedef " << nstruct() << " N;\ntypedef N::S S;\ntypedef N::C C;\ntypedef N::A A;\n";
+    os << "#define NT " << NT << "\n";
+    os << "extern \"C\" __global__ void __launch_bounds__(NT)";
+    if (CL > 1) os << " __cluster_dims__(" << CL << ", 1, 1)";
+    os << " @KNAME@(const sgm::Args a) {\n";
+    os << "  extern __shared__ __align__(128) unsigned char sm[];\n";
+    os << "  const int tid = threadIdx.x;\n";
+    os << "  const long long bid = blockIdx.x;\n";
+    if (CL > 1) os << "  const unsigned crank = sgm::cluster_rank();\n";
+    else os << "  const unsigned crank = 0u; (void)crank;\n";
+    os << "  long long rest = bid / " << CL << ";\n";
+    os << "  const long long fpart = rest % " << FP << "; rest /= " << FP << "; (void)fpart;\n";
+    static const char* gv[3] = {"gx", "gy", "gz"};
+    for (int g = 0; g < ngrid; ++g)
+      os << "  const long long " << gv[g] << " = rest % " << grid[g] << "; rest /= " << grid[g] << "; (void)" << gv[g]
+         << ";\n";
+    for (int c = 0; c < (int)cls.size(); ++c) {
+      if (cls[c].parts <= 1) continue;
+      if (cls[c].cluster)
+        os << "  const int " << part_var(c) << " = (int)((crank >> " << cls[c].bit_shift << ") & " << (cls[c].parts - 1)
+           << "u);\n";
+      else
+        os << "  const int " << part_var(c) << " = (int)((fpart / " << cls[c].radix << "LL) % " << cls[c].parts
+           << "LL);\n";
+    }
+    if (LP > 1) os << "  const int jp = (int)((crank >> " << loop_shift << ") & " << (LP - 1) << "u);\n";
+    else os << "  const int jp = 0; (void)jp;\n";
+    if (scratch_per_cta > 0)
+      os << "  unsigned char* scr = (unsigned char*)a.scratch + bid * " << scratch_per_cta << "LL;\n";
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      const Node& x = nodes[n];
+      if (x.store == ST_SMEM && x.kind != SGM_OUTPUT)
+        os << "  C* " << tile_ptr(n) << " = (C*)(sm + " << x.off << ");\n";
+      else if (x.store == ST_GLOBAL)
+        os << "  C* " << tile_ptr(n) << " = (C*)(scr + " << x.off << ");\n";
+    }
+    bool in_loop = false;
+    for (int p = 0; p < (int)sched.size(); ++p) {
+      const Ev& e = sched[p];
+      if (e.type == Ev::LOOP_BEGIN) {
+        for (int n = 0; n < (int)nodes.size(); ++n)
+          if (nodes[n].kind == SGM_ACCUM)
+            os << "  for (int e = tid; e < " << prod4(nodes[n].sl) << "; e += NT) " << tile_ptr(n) << "[e] = N::zero();\n";
+        os << "  __syncthreads();\n";
+        os << "  for (int j = jp; j < " << nloop << "; j += " << LP << ") {\n";
+        in_loop = true;
+      } else if (e.type == Ev::LOOP_END) {
+        os << "  }\n";
+        in_loop = false;
+      } else if (e.type == Ev::FLUSH) {
+        emit_flush(e.flush, p);
+      } else {
+        emit_node(e.node, in_loop);
+      }
+    }
+    os << "}\n";
+  }
+
+  GenResult run() {
+    if (!load() || !shapes()) return R;
+    structure();
+    decide_views();
+    split_plan();
+    if (!fit()) {
+      // still over budget after spilling everything spillable
+      if (smem_peak > 227 * 1024) {
+        fail(SGM_ERR_RESOURCE, "shared memory plan exceeds 227 KB");
+        return R;
+      }
+    }
+    emit();
+    std::string src = os.str();
+    uint64_t h = fnv1a(src);
+    char name[64];
+    snprintf(name, sizeof name, "sgm_cand_%016" PRIx64, h);
+    R.kernel_name = name;
+    size_t at = src.find("@KNAME@");
+    if (at != std::string::npos) src.replace(at, 7, name);
+    R.source = src;
+    R.logical_blocks = LB;
+    R.cluster = CL;
+    R.free_parts = FP;
+    R.ctas = LB * FP * CL;
+    R.threads = NT;
+    R.smem_bytes = smem_peak;
+    R.loop_parts = LP;
+    R.scratch_bytes = scratch_per_cta * R.ctas;
+    std::ostringstream s;
+    s << "LB=" << LB << " FP=" << FP << " CL=" << CL << " LP=" << LP << " smem=" << smem_peak
+      << " scratch/cta=" << scratch_per_cta << " classes:";
+    for (int c = 0; c < (int)cls.size(); ++c)
+      s << " c" << c << "(" << cls[c].extent << (cls[c].reduced ? "r" : "f") << "/" << cls[c].parts << ")";
+    s << " mm:";
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (nodes[n].kind == SGM_MATMUL) s << " n" << n << (nodes[n].gemv ? "gemv" : "gen") << (nodes[n].gemv ? "/vn" + std::to_string(nodes[n].vn) + "ks" + std::to_string(nodes[n].ks) : "");
+    R.summary = s.str();
+    return R;
+  }
+};
+
+}  // namespace
+
+GenResult generate(const sgm_plan_desc& desc, int num_sms) {
+  Gen g(desc, num_sms > 0 ? num_sms : 148);
+  return g.run();
+}
+
+}  // namespace sgmcg

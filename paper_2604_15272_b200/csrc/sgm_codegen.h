@@ -1,0 +1,37 @@
+// sgm_codegen.h — planner + CUDA code generator for instantiated sGraph candidates.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sgm.h"
+
+namespace sgmcg {
+
+struct GenResult {
+  int status = SGM_OK;
+  std::string error;
+  std::string source;       // CUDA C++ for NVRTC
+  std::string kernel_name;  // extern "C" entry
+  int64_t logical_blocks = 1;
+  int64_t ctas = 1;
+  int cluster = 1;
+  int threads = 256;
+  int smem_bytes = 0;
+  int loop_parts = 1;
+  int64_t free_parts = 1;
+  int64_t scratch_bytes = 0;   // total global scratch (all CTAs)
+  int n_tcgen05 = 0;
+  std::string summary;
+};
+
+// Validate the descriptor, derive tile shapes from the mapping exactly as the
+// reference interpreter slices (interp.py:90-125), plan the CTA/cluster
+// decomposition and emit the kernel source.
+GenResult generate(const sgm_plan_desc& desc, int num_sms);
+
+// Helpers shared with the runtime.
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull);
+uint32_t ff_const(int64_t num, int64_t den);  // num * den^-1 mod 2^31-1
+
+}  // namespace sgmcg

@@ -1,0 +1,480 @@
+// sgm_dev.cuh — device building blocks for generated sGraph-candidate kernels.
+//
+// Every generated kernel (sgm_codegen.cpp) includes this header through NVRTC.
+// A kernel executes one *logical block* of the candidate's block graph with one
+// CTA, or with several CTAs: "free parts" (independent CTAs splitting an axis
+// no node reduces) and "cluster parts" (CTAs of one thread-block cluster that
+// split a reduced axis or the for-loop and combine partial tiles through
+// distributed shared memory).  Tiles live in shared memory as dense row-major
+// rank-4 arrays of the number system's compute type.
+//
+// Semantics follow the reference interpreter (pkg/src/symfuse/interp.py):
+//   apply_op (interp.py:45-66)   -> unary/binary/sum/matmul/scale below
+//   _silu    (interp.py:36-42)   -> NF64::silu / NF32::silu (same two branches)
+//   accum    (interp.py:171-176) -> plain sums (order-insensitive up to fp rounding)
+// and the finite-field restatement in oracle/ff_np.py (bit-exact).
+#pragma once
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+typedef long long i64;
+typedef unsigned short u16;
+
+namespace sgm {
+
+struct Args {
+  const void* in[16];
+  void* out[16];
+  void* scratch;
+};
+
+// ---------------------------------------------------------------------------
+// Finite field GF(p), p = 2^31 - 1 (Mersenne): 2^31 == 1 (mod p).
+
+constexpr u32 P = 0x7FFFFFFFu;
+
+__device__ __forceinline__ u32 modp64(u64 v) {
+  v = (v & P) + (v >> 31);
+  v = (v & P) + (v >> 31);
+  u32 r = (u32)v;
+  return r >= P ? r - P : r;
+}
+__device__ __forceinline__ u32 ff_add(u32 a, u32 b) { u32 s = a + b; return s >= P ? s - P : s; }
+__device__ __forceinline__ u32 ff_mul(u32 a, u32 b) { return modp64((u64)a * b); }
+// product folded below 2^32 (lazy reduction for dot products)
+__device__ __forceinline__ u64 ff_mul_lazy(u32 a, u32 b) { u64 x = (u64)a * b; return (x & P) + (x >> 31); }
+__device__ __forceinline__ u32 ff_inv(u32 a) {
+  // a^(p-2); inv(0) := 0 (documented convention, mirrored in oracle/ff_np.py)
+  u32 r = 1, b = a;
+  u32 e = P - 2u;
+  while (e) {
+    if (e & 1u) r = ff_mul(r, b);
+    b = ff_mul(b, b);
+    e >>= 1;
+  }
+  return r;
+}
+__device__ __forceinline__ u64 mix64(u64 z) {
+  z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ULL;
+  z ^= z >> 27; z *= 0x94d049bb133111ebULL;
+  z ^= z >> 31;
+  return z;
+}
+// Uninterpreted unary ops as keyed hashes: h_k(x) = mix64(x + K_k) mod p.
+constexpr u64 FF_KEY_EXP = 0x9E3779B97F4A7C15ULL;
+constexpr u64 FF_KEY_SILU = 0x3C6EF372FE94F82AULL;
+constexpr u64 FF_KEY_SQRT = 0xDAA66D2C7DDF743FULL;
+__device__ __forceinline__ u32 ff_hash(u32 x, u64 key) { return modp64(mix64((u64)x + key)); }
+
+// ---------------------------------------------------------------------------
+// Number systems.  S = storage type in HBM, C = tile (compute) type in smem,
+// A = accumulator type for reductions (sum / matmul contraction).
+
+struct NF64 {
+  typedef double S; typedef double C; typedef double A;
+  static constexpr int VEC = 2;  // elements per 16-byte vector
+  __device__ static __forceinline__ C ld(S v) { return v; }
+  __device__ static __forceinline__ S st(C v) { return v; }
+  __device__ static __forceinline__ C zero() { return 0.0; }
+  __device__ static __forceinline__ C nan() { return __longlong_as_double(0x7ff8000000000000LL); }
+  __device__ static __forceinline__ C add(C a, C b) { return a + b; }
+  __device__ static __forceinline__ C mul(C a, C b) { return a * b; }
+  __device__ static __forceinline__ C div(C a, C b) { return a / b; }
+  __device__ static __forceinline__ C sq(C a) { return a * a; }
+  __device__ static __forceinline__ C ex(C a) { return ::exp(a); }
+  __device__ static __forceinline__ C sqr(C a) { return ::sqrt(a); }
+  __device__ static __forceinline__ C silu(C x) {
+    if (x >= 0.0) return x / (1.0 + ::exp(-x));
+    C e = ::exp(x);
+    return x * e / (1.0 + e);
+  }
+  __device__ static __forceinline__ C scale(C x, C c) { return c * x; }
+  __device__ static __forceinline__ A azero() { return 0.0; }
+  __device__ static __forceinline__ void aadd(A& a, C v) { a += v; }
+  __device__ static __forceinline__ void amerge(A& a, A b) { a += b; }
+  __device__ static __forceinline__ void mac(A& a, C x, C y) { a = fma(x, y, a); }
+  __device__ static __forceinline__ C fin(A a) { return a; }
+};
+
+struct NF32 {
+  typedef float S; typedef float C; typedef float A;
+  static constexpr int VEC = 4;
+  __device__ static __forceinline__ C ld(S v) { return v; }
+  __device__ static __forceinline__ S st(C v) { return v; }
+  __device__ static __forceinline__ C zero() { return 0.0f; }
+  __device__ static __forceinline__ C nan() { return __int_as_float(0x7fc00000); }
+  __device__ static __forceinline__ C add(C a, C b) { return a + b; }
+  __device__ static __forceinline__ C mul(C a, C b) { return a * b; }
+  __device__ static __forceinline__ C div(C a, C b) { return a / b; }
+  __device__ static __forceinline__ C sq(C a) { return a * a; }
+  __device__ static __forceinline__ C ex(C a) { return expf(a); }
+  __device__ static __forceinline__ C sqr(C a) { return sqrtf(a); }
+  __device__ static __forceinline__ C silu(C x) {
+    if (x >= 0.0f) return x / (1.0f + expf(-x));
+    C e = expf(x);
+    return x * e / (1.0f + e);
+  }
+  __device__ static __forceinline__ C scale(C x, C c) { return c * x; }
+  __device__ static __forceinline__ A azero() { return 0.0f; }
+  __device__ static __forceinline__ void aadd(A& a, C v) { a += v; }
+  __device__ static __forceinline__ void amerge(A& a, A b) { a += b; }
+  __device__ static __forceinline__ void mac(A& a, C x, C y) { a = fmaf(x, y, a); }
+  __device__ static __forceinline__ C fin(A a) { return a; }
+};
+
+// bf16 storage (raw bits), fp32 compute; round-to-nearest-even on store.
+struct NBF16 : NF32 {
+  typedef u16 S;
+  static constexpr int VEC = 8;
+  __device__ static __forceinline__ C ld(S v) { return __uint_as_float(((u32)v) << 16); }
+  __device__ static __forceinline__ S st(C f) {
+    u32 u = __float_as_uint(f);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (S)0x7fc0;
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (S)(u >> 16);
+  }
+};
+
+struct NFF {
+  typedef u32 S; typedef u32 C; typedef u64 A;
+  static constexpr int VEC = 4;
+  __device__ static __forceinline__ C ld(S v) { return v; }
+  __device__ static __forceinline__ S st(C v) { return v; }
+  __device__ static __forceinline__ C zero() { return 0u; }
+  __device__ static __forceinline__ C nan() { return 0xFFFFFFFFu; }  // not a residue
+  __device__ static __forceinline__ C add(C a, C b) { return ff_add(a, b); }
+  __device__ static __forceinline__ C mul(C a, C b) { return ff_mul(a, b); }
+  __device__ static __forceinline__ C div(C a, C b) { return ff_mul(a, ff_inv(b)); }
+  __device__ static __forceinline__ C sq(C a) { return ff_mul(a, a); }
+  __device__ static __forceinline__ C ex(C a) { return ff_hash(a, FF_KEY_EXP); }
+  __device__ static __forceinline__ C sqr(C a) { return ff_hash(a, FF_KEY_SQRT); }
+  __device__ static __forceinline__ C silu(C a) { return ff_hash(a, FF_KEY_SILU); }
+  __device__ static __forceinline__ C scale(C x, C c) { return ff_mul(c, x); }
+  __device__ static __forceinline__ A azero() { return 0ull; }
+  __device__ static __forceinline__ void aadd(A& a, C v) { a += v; }      // < 2^31 per term
+  __device__ static __forceinline__ void amerge(A& a, A b) { a += b; }
+  __device__ static __forceinline__ void mac(A& a, C x, C y) { a += ff_mul_lazy(x, y); }  // < 2^32 per term
+  __device__ static __forceinline__ C fin(A a) { return modp64(a); }
+};
+
+// Storage -> compute conversion usable on either a smem tile (C) or a global view (S).
+template <class X, class Y> struct same_t { static constexpr bool v = false; };
+template <class X> struct same_t<X, X> { static constexpr bool v = true; };
+template <class N, class T> __device__ __forceinline__ typename N::C cvs(T v) {
+  if constexpr (same_t<T, typename N::C>::v) return v;
+  else return N::ld(v);
+}
+
+// ---------------------------------------------------------------------------
+// Warp / cluster primitives
+
+__device__ __forceinline__ u32 cluster_rank() {
+  u32 r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class T> __device__ __forceinline__ const T* peer_ptr(const T* p, u32 rank) {
+  u64 out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"((u64)p), "r"(rank));
+  return (const T*)out;
+}
+
+template <class T> __device__ __forceinline__ T shfl_xor(T v, int off, u32 mask) {
+  return __shfl_xor_sync(mask, v, off);
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_stream8(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Tile movement: strided rank-4 global view <-> dense smem tile.
+// VEC > 1 only when the planner proved 16-byte alignment of every row start.
+
+template <class N, int D0, int D1, int D2, int D3, i64 S0, i64 S1, i64 S2, i64 S3, int VEC, int NT>
+__device__ __forceinline__ void load_tile(typename N::C* __restrict__ dst, const typename N::S* __restrict__ src) {
+  typedef typename N::S S;
+  constexpr int ROWS = D0 * D1 * D2;
+  if constexpr (VEC > 1) {
+    constexpr int V3 = D3 / VEC;
+    for (int e = threadIdx.x; e < ROWS * V3; e += NT) {
+      const int v = e % V3;
+      const int r = e / V3;
+      const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
+      const S* p = src + i0 * S0 + i1 * S1 + i2 * S2 + (i64)v * VEC;
+      union { uint4 q; S s[VEC]; } u;
+      u.q = *reinterpret_cast<const uint4*>(p);
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) dst[r * D3 + v * VEC + t] = N::ld(u.s[t]);
+    }
+  } else {
+    for (int e = threadIdx.x; e < ROWS * D3; e += NT) {
+      const int i3 = e % D3;
+      const int r = e / D3;
+      const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
+      dst[e] = N::ld(src[i0 * S0 + i1 * S1 + i2 * S2 + (i64)i3 * S3]);
+    }
+  }
+}
+
+template <class N, int D0, int D1, int D2, int D3, i64 S0, i64 S1, i64 S2, i64 S3, int VEC, int NT>
+__device__ __forceinline__ void store_tile(typename N::S* __restrict__ dst, const typename N::C* __restrict__ src) {
+  typedef typename N::S S;
+  constexpr int ROWS = D0 * D1 * D2;
+  if constexpr (VEC > 1) {
+    constexpr int V3 = D3 / VEC;
+    for (int e = threadIdx.x; e < ROWS * V3; e += NT) {
+      const int v = e % V3;
+      const int r = e / V3;
+      const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
+      union { uint4 q; S s[VEC]; } u;
+#pragma unroll
+      for (int t = 0; t < VEC; ++t) u.s[t] = N::st(src[r * D3 + v * VEC + t]);
+      *reinterpret_cast<uint4*>(dst + i0 * S0 + i1 * S1 + i2 * S2 + (i64)v * VEC) = u.q;
+    }
+  } else {
+    for (int e = threadIdx.x; e < ROWS * D3; e += NT) {
+      const int i3 = e % D3;
+      const int r = e / D3;
+      const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
+      dst[i0 * S0 + i1 * S1 + i2 * S2 + (i64)i3 * S3] = N::st(src[e]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sum over one axis (keepdims).  TPO threads cooperate on each output value.
+
+template <int A, int B> struct cmin { static constexpr int v = A < B ? A : B; };
+__host__ __device__ constexpr int pow2_floor(int x) { int p = 1; while (p * 2 <= x) p *= 2; return p; }
+__host__ __device__ constexpr int pow2_ceil(int x) { int p = 1; while (p < x) p *= 2; return p; }
+
+template <class N, int D0, int D1, int D2, int D3, int AX, int NT>
+__device__ __forceinline__ void sum_axis(typename N::C* __restrict__ dst, const typename N::C* __restrict__ src) {
+  typedef typename N::A Acc;
+  constexpr int DIMS[4] = {D0, D1, D2, D3};
+  constexpr int L = DIMS[AX];
+  constexpr int INNER = (AX == 0 ? D1 * D2 * D3 : AX == 1 ? D2 * D3 : AX == 2 ? D3 : 1);
+  constexpr int OUT = D0 * D1 * D2 * D3 / L;
+  constexpr int TPO0 = pow2_floor(NT / OUT > 0 ? NT / OUT : 1);
+  constexpr int TPO = TPO0 > pow2_ceil(L) ? pow2_ceil(L) : TPO0;  // threads per output
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x;
+  if constexpr (TPO <= 32) {
+    constexpr int GROUPS = NT / TPO;
+    const int lane = tid & 31;
+    const u32 gmask = (TPO == 32) ? 0xffffffffu : (((1u << TPO) - 1u) << (lane & ~(TPO - 1)));
+    for (int o = tid / TPO; o < OUT; o += GROUPS) {
+      const int outer = o / INNER, inner = o % INNER;
+      const typename N::C* p = src + outer * (L * INNER) + inner;
+      Acc acc = N::azero();
+      for (int k = tid % TPO; k < L; k += TPO) N::aadd(acc, p[k * INNER]);
+#pragma unroll
+      for (int off = TPO / 2; off > 0; off >>= 1) N::amerge(acc, shfl_xor(acc, off, gmask));
+      if ((tid % TPO) == 0) dst[o] = N::fin(acc);
+    }
+  } else {
+    // OUT < NW: several warps per output, combined through smem.
+    constexpr int WPO = TPO / 32;
+    __shared__ Acc part[NW];
+    const int w = tid >> 5, lane = tid & 31;
+    const int o = w / WPO;
+    Acc acc = N::azero();
+    if (o < OUT) {
+      const int outer = o / INNER, inner = o % INNER;
+      const typename N::C* p = src + outer * (L * INNER) + inner;
+      for (int k = (w % WPO) * 32 + lane; k < L; k += TPO) N::aadd(acc, p[k * INNER]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) N::amerge(acc, shfl_xor(acc, off, 0xffffffffu));
+    if (lane == 0) part[w] = acc;
+    __syncthreads();
+    if (tid < OUT) {
+      Acc t = N::azero();
+      for (int q = 0; q < WPO; ++q) N::amerge(t, part[tid * WPO + q]);
+      dst[tid] = N::fin(t);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic batched contraction: out[b0][b1][m][n] = sum_k A(b0,b1,m,k) * B(b0,b1,k,n).
+// A and B are either smem tiles (TA/TB = N::C) or global views (N::S), given by
+// compile-time strides (0 for broadcast dims).  TPO lanes split k.
+
+template <class N, class TA, class TB, int B0, int B1, int M, int K, int NN,
+          i64 SA0, i64 SA1, i64 SA2, i64 SA3, i64 SB0, i64 SB1, i64 SB2, i64 SB3, int NT>
+__device__ __forceinline__ void mm_generic(typename N::C* __restrict__ out, const TA* __restrict__ A,
+                                           const TB* __restrict__ B) {
+  typedef typename N::A Acc;
+  constexpr int OUT = B0 * B1 * M * NN;
+  constexpr int TPO0 = pow2_floor(NT / OUT > 0 ? NT / OUT : 1);
+  constexpr int TPO1 = TPO0 > 32 ? 32 : TPO0;
+  constexpr int TPO = TPO1 > pow2_ceil(K) ? pow2_ceil(K) : TPO1;
+  constexpr int GROUPS = NT / TPO;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const u32 gmask = (TPO == 32) ? 0xffffffffu : (((1u << TPO) - 1u) << (lane & ~(TPO - 1)));
+  for (int o = tid / TPO; o < OUT; o += GROUPS) {
+    const int n = o % NN;
+    int r = o / NN;
+    const int m = r % M; r /= M;
+    const int b1 = r % B1, b0 = r / B1;
+    const TA* pa = A + b0 * SA0 + b1 * SA1 + (i64)m * SA2;
+    const TB* pb = B + b0 * SB0 + b1 * SB1 + (i64)n * SB3;
+    Acc acc = N::azero();
+    for (int k = tid % TPO; k < K; k += TPO) N::mac(acc, cvs<N>(pa[(i64)k * SA3]), cvs<N>(pb[(i64)k * SB2]));
+#pragma unroll
+    for (int off = TPO / 2; off > 0; off >>= 1) N::amerge(acc, shfl_xor(acc, off, gmask));
+    if ((tid % TPO) == 0) out[o] = N::fin(acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Streamed GEMV-like contraction: A small in smem ([B0][B1][M][K], strides SA*),
+// B a global view streamed once (row k contiguous along n), output [B0][B1][M][NN].
+// Work item = (batch, vector of VN columns); KS threads split k (interleaved),
+// partials combined with warp shuffles (ks lanes inside a warp) then smem.
+// `red` is a smem scratch of at least red_elems() accumulators.
+
+template <int NV, int KS, bool SHFL> struct gemv_layout {
+  // lanes: t = nv + NV*ks + NV*KS*item_hi
+  static constexpr int KS_IN_WARP = (!SHFL || NV >= 32) ? 1 : ((32 / NV) < KS ? (32 / NV) : KS);
+  static constexpr int KS_OUT = KS / KS_IN_WARP;
+};
+
+template <class N, class TB, int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3,
+          i64 SB0, i64 SB1, i64 SB2, int VN, int KS, int UNR, bool SHFL, int NT>
+__device__ __forceinline__ void mm_gemv(typename N::C* __restrict__ out, const typename N::C* __restrict__ A,
+                                        const TB* __restrict__ B, typename N::A* __restrict__ red) {
+  typedef typename N::A Acc;
+  typedef typename N::C C;
+  constexpr int NV = NN / VN;
+  constexpr int ITEMS = B0 * B1 * NV;
+  constexpr int WORK = ITEMS * KS;
+  typedef gemv_layout<NV, KS, SHFL> LY;
+  static_assert(NN % VN == 0, "VN must divide NN");
+  const int tid = threadIdx.x;
+  for (int w = tid; w < WORK; w += NT) {
+    const int nv = w % NV;
+    const int ks = (w / NV) % KS;
+    const int bi = w / (NV * KS);
+    const int b1 = bi % B1, b0 = bi / B1;
+    const C* pa = A + b0 * SA0 + b1 * SA1;
+    const TB* pb = B + b0 * SB0 + b1 * SB1 + nv * VN;
+    Acc acc[M][VN];
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+#pragma unroll
+      for (int v = 0; v < VN; ++v) acc[m][v] = N::azero();
+    constexpr int STEP = KS * UNR;
+    for (int k0 = ks; k0 < K; k0 += STEP) {
+      TB bv[UNR][VN];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int k = k0 + u * KS;
+        if (K % STEP == 0 || k < K) {
+          const TB* src = pb + (i64)k * SB2;
+          if constexpr (sizeof(TB) * VN == 16) {
+            union { uint4 q; TB s[VN]; } t; t.q = ldg_stream(src);
+#pragma unroll
+            for (int v = 0; v < VN; ++v) bv[u][v] = t.s[v];
+          } else if constexpr (sizeof(TB) * VN == 8) {
+            union { uint2 q; TB s[VN]; } t; t.q = ldg_stream8(src);
+#pragma unroll
+            for (int v = 0; v < VN; ++v) bv[u][v] = t.s[v];
+          } else {
+#pragma unroll
+            for (int v = 0; v < VN; ++v) bv[u][v] = src[v];
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < VN; ++v) bv[u][v] = TB(0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int k = k0 + u * KS;
+        if (K % STEP == 0 || k < K) {
+          C bc[VN];
+#pragma unroll
+          for (int v = 0; v < VN; ++v) bc[v] = cvs<N>(bv[u][v]);
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            const C a = pa[m * SA2 + (i64)k * SA3];
+#pragma unroll
+            for (int v = 0; v < VN; ++v) N::mac(acc[m][v], a, bc[v]);
+          }
+        }
+      }
+    }
+    // reduce the KS_IN_WARP partials living in one warp (lanes NV apart)
+    if constexpr (LY::KS_IN_WARP > 1) {
+#pragma unroll
+      for (int off = NV * LY::KS_IN_WARP / 2; off >= NV; off >>= 1)
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int v = 0; v < VN; ++v) N::amerge(acc[m][v], shfl_xor(acc[m][v], off, 0xffffffffu));
+    }
+    const int ksw = ks % LY::KS_IN_WARP;
+    if constexpr (LY::KS_OUT == 1) {
+      if (ksw == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int v = 0; v < VN; ++v) out[((i64)bi * M + m) * NN + nv * VN + v] = N::fin(acc[m][v]);
+      }
+    } else {
+      if (ksw == 0) {
+        const int kso = ks / LY::KS_IN_WARP;
+        const int item = bi * NV + nv;
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int v = 0; v < VN; ++v) red[(((i64)kso * ITEMS + item) * M + m) * VN + v] = acc[m][v];
+      }
+    }
+  }
+  if constexpr (LY::KS_OUT > 1) {
+    __syncthreads();
+    for (int e = tid; e < ITEMS * M * VN; e += NT) {
+      Acc t = N::azero();
+#pragma unroll 4
+      for (int q = 0; q < LY::KS_OUT; ++q) N::amerge(t, red[(i64)q * ITEMS * M * VN + e]);
+      const int v = e % VN;
+      const int m = (e / VN) % M;
+      const int item = e / (VN * M);
+      const int nv = item % NV, bi = item / NV;
+      out[((i64)bi * M + m) * NN + nv * VN + v] = N::fin(t);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster all-reduce of a partial tile: tmp[e] = sum over peers r with
+// ((r ^ me) & KEEP) == 0 of tile_r[e], in rank order (identical on every CTA).
+
+template <class N, int SZ, int CL, u32 KEEP, int NT>
+__device__ __forceinline__ void cl_reduce(const typename N::C* tile, typename N::C* tmp, u32 me) {
+  typedef typename N::A Acc;
+  for (int e = threadIdx.x; e < SZ; e += NT) {
+    Acc acc = N::azero();
+#pragma unroll
+    for (u32 r = 0; r < (u32)CL; ++r)
+      if (((r ^ me) & KEEP) == 0u) N::aadd(acc, peer_ptr(tile, r)[e]);
+    tmp[e] = N::fin(acc);
+  }
+}
+
+}  // namespace sgm

@@ -1,0 +1,659 @@
+// sgm_runtime.cpp — C-ABI runtime of libsgm.so (see include/sgm.h).
+//
+// * CUDA driver API resolved with dlopen("libcuda.so.1") at sgm_init, so the
+//   library loads (and exports its symbols) on a machine without a GPU.
+// * Kernels are generated per candidate (sgm_codegen.cpp), compiled with NVRTC
+//   for sm_100a and cached on disk as cubins keyed by a hash of the source, so
+//   re-runs and multi-rank sweeps are compile-free (checkpoint/resume of tuning).
+// * Timing uses CUDA events around a CUDA graph of back-to-back launches with
+//   rotating input sets (inputs miss L2 between launches).
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <cinttypes>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/sgm.h"
+#include "sgm_codegen.h"
+
+namespace sgm {
+// host mirror of sgm::Args in sgm_dev.cuh (kernel parameter block)
+struct Args {
+  const void* in[16];
+  void* out[16];
+  void* scratch;
+};
+}  // namespace sgm
+
+namespace {
+
+const char* kDevHeader =
+#include "sgm_dev_embed.inc"
+    ;
+const char* kUtilHeader =
+#include "sgm_util_embed.inc"
+    ;
+
+thread_local std::string g_err;
+
+int set_err(int st, const char* fmt, ...) {
+  char buf[2048];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+// ---------------------------------------------------------------- driver API
+struct Driver {
+  bool ok = false;
+  void* h = nullptr;
+#define SGM_FN(name, ...) CUresult (*name)(__VA_ARGS__) = nullptr;
+  SGM_FN(cuInit, unsigned)
+  SGM_FN(cuDeviceGet, CUdevice*, int)
+  SGM_FN(cuDeviceGetAttribute, int*, CUdevice_attribute, CUdevice)
+  SGM_FN(cuDevicePrimaryCtxRetain, CUcontext*, CUdevice)
+  SGM_FN(cuCtxSetCurrent, CUcontext)
+  SGM_FN(cuCtxGetCurrent, CUcontext*)
+  SGM_FN(cuModuleLoadData, CUmodule*, const void*)
+  SGM_FN(cuModuleUnload, CUmodule)
+  SGM_FN(cuModuleGetFunction, CUfunction*, CUmodule, const char*)
+  SGM_FN(cuFuncSetAttribute, CUfunction, CUfunction_attribute, int)
+  SGM_FN(cuLaunchKernel, CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+         void**, void**)
+  SGM_FN(cuMemAlloc, CUdeviceptr*, size_t)
+  SGM_FN(cuMemFree, CUdeviceptr)
+  SGM_FN(cuMemHostAlloc, void**, size_t, unsigned)
+  SGM_FN(cuMemFreeHost, void*)
+  SGM_FN(cuMemcpyHtoDAsync, CUdeviceptr, const void*, size_t, CUstream)
+  SGM_FN(cuMemcpyDtoHAsync, void*, CUdeviceptr, size_t, CUstream)
+  SGM_FN(cuMemsetD32Async, CUdeviceptr, unsigned, size_t, CUstream)
+  SGM_FN(cuStreamSynchronize, CUstream)
+  SGM_FN(cuStreamCreate, CUstream*, unsigned)
+  SGM_FN(cuStreamDestroy, CUstream)
+  SGM_FN(cuEventCreate, CUevent*, unsigned)
+  SGM_FN(cuEventDestroy, CUevent)
+  SGM_FN(cuEventRecord, CUevent, CUstream)
+  SGM_FN(cuEventSynchronize, CUevent)
+  SGM_FN(cuEventElapsedTime, float*, CUevent, CUevent)
+  SGM_FN(cuStreamBeginCapture, CUstream, CUstreamCaptureMode)
+  SGM_FN(cuStreamEndCapture, CUstream, CUgraph*)
+  SGM_FN(cuGraphInstantiateWithFlags, CUgraphExec*, CUgraph, unsigned long long)
+  SGM_FN(cuGraphLaunch, CUgraphExec, CUstream)
+  SGM_FN(cuGraphExecDestroy, CUgraphExec)
+  SGM_FN(cuGraphDestroy, CUgraph)
+  SGM_FN(cuOccupancyMaxActiveClusters, int*, CUfunction, const CUlaunchConfig*)
+#undef SGM_FN
+  CUresult (*cuGetErrorString)(CUresult, const char**) = nullptr;
+
+  template <class F> bool sym(F& f, const char* a, const char* b = nullptr) {
+    void* p = dlsym(h, a);
+    if (!p && b) p = dlsym(h, b);
+    f = reinterpret_cast<F>(p);
+    return p != nullptr;
+  }
+  bool load() {
+    if (ok) return true;
+    h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libcuda.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    bool g = true;
+    g &= sym(cuInit, "cuInit");
+    g &= sym(cuDeviceGet, "cuDeviceGet");
+    g &= sym(cuDeviceGetAttribute, "cuDeviceGetAttribute");
+    g &= sym(cuDevicePrimaryCtxRetain, "cuDevicePrimaryCtxRetain");
+    g &= sym(cuCtxSetCurrent, "cuCtxSetCurrent");
+    g &= sym(cuCtxGetCurrent, "cuCtxGetCurrent");
+    g &= sym(cuModuleLoadData, "cuModuleLoadData");
+    g &= sym(cuModuleUnload, "cuModuleUnload");
+    g &= sym(cuModuleGetFunction, "cuModuleGetFunction");
+    g &= sym(cuFuncSetAttribute, "cuFuncSetAttribute");
+    g &= sym(cuLaunchKernel, "cuLaunchKernel");
+    g &= sym(cuMemAlloc, "cuMemAlloc_v2");
+    g &= sym(cuMemFree, "cuMemFree_v2");
+    g &= sym(cuMemHostAlloc, "cuMemHostAlloc");
+    g &= sym(cuMemFreeHost, "cuMemFreeHost");
+    g &= sym(cuMemcpyHtoDAsync, "cuMemcpyHtoDAsync_v2");
+    g &= sym(cuMemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2");
+    g &= sym(cuMemsetD32Async, "cuMemsetD32Async");
+    g &= sym(cuStreamSynchronize, "cuStreamSynchronize");
+    g &= sym(cuStreamCreate, "cuStreamCreate");
+    g &= sym(cuStreamDestroy, "cuStreamDestroy_v2");
+    g &= sym(cuEventCreate, "cuEventCreate");
+    g &= sym(cuEventDestroy, "cuEventDestroy_v2");
+    g &= sym(cuEventRecord, "cuEventRecord");
+    g &= sym(cuEventSynchronize, "cuEventSynchronize");
+    g &= sym(cuEventElapsedTime, "cuEventElapsedTime");
+    g &= sym(cuStreamBeginCapture, "cuStreamBeginCapture_v2");
+    g &= sym(cuStreamEndCapture, "cuStreamEndCapture");
+    g &= sym(cuGraphInstantiateWithFlags, "cuGraphInstantiateWithFlags");
+    g &= sym(cuGraphLaunch, "cuGraphLaunch");
+    g &= sym(cuGraphExecDestroy, "cuGraphExecDestroy");
+    g &= sym(cuGraphDestroy, "cuGraphDestroy");
+    sym(cuOccupancyMaxActiveClusters, "cuOccupancyMaxActiveClusters");
+    sym(cuGetErrorString, "cuGetErrorString");
+    ok = g;
+    return ok;
+  }
+};
+Driver D;
+std::mutex g_init_mu;
+
+struct DevState {
+  bool init = false;
+  CUdevice dev = 0;
+  CUcontext ctx = nullptr;
+  int sms = 148;
+  int cc_major = 10, cc_minor = 0;
+  CUmodule util = nullptr;
+  CUfunction f_fill64, f_fill32, f_fill16, f_ff_fill, f_cmp, f_re64, f_re32, f_re16, f_n64, f_n32, f_n16;
+  CUdeviceptr red = 0;  // 4 x u64 reduction scratch
+};
+DevState g_dev[16];
+thread_local int t_device = -1;
+std::string g_cache_dir;
+std::mutex g_cache_mu;
+
+int cu_check(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return SGM_OK;
+  const char* s = "?";
+  if (D.cuGetErrorString) D.cuGetErrorString(r, &s);
+  return set_err(SGM_ERR_CUDA, "%s failed: %s (%d)", what, s, (int)r);
+}
+#define CU(call)                                            \
+  do {                                                      \
+    int _st = cu_check((call), #call);                      \
+    if (_st != SGM_OK) return _st;                          \
+  } while (0)
+
+std::string default_cache_dir() {
+  if (const char* e = getenv("SGM_CACHE_DIR")) return e;
+  Dl_info info;
+  if (dladdr((void*)&default_cache_dir, &info) && info.dli_fname) {
+    std::string p = info.dli_fname;
+    size_t at = p.find_last_of('/');
+    if (at != std::string::npos) return p.substr(0, at) + "/.cubin_cache";
+  }
+  return "/tmp/sgm_cubin_cache";
+}
+
+std::string cache_dir() {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (g_cache_dir.empty()) g_cache_dir = default_cache_dir();
+  return g_cache_dir;
+}
+
+bool read_file(const std::string& path, std::string& out) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  std::ostringstream ss;
+  ss << f.rdbuf();
+  out = ss.str();
+  return !out.empty();
+}
+
+void write_file_atomic(const std::string& path, const std::string& data) {
+  std::string dir = path.substr(0, path.find_last_of('/'));
+  mkdir(dir.c_str(), 0755);
+  char tmp[64];
+  snprintf(tmp, sizeof tmp, ".tmp.%d.%p", (int)getpid(), (void*)&data);
+  std::string t = path + tmp;
+  {
+    std::ofstream f(t, std::ios::binary);
+    if (!f) return;
+    f.write(data.data(), (std::streamsize)data.size());
+  }
+  rename(t.c_str(), path.c_str());
+}
+
+const char* kArch = "-arch=sm_100a";
+
+// Compile `src` (which #includes sgm_dev.cuh / sgm_util.cuh) to a cubin, with the disk cache.
+int compile_cubin(const std::string& src, std::string& cubin, double& ms, int& hit) {
+  int maj = 0, minr = 0;
+  nvrtcVersion(&maj, &minr);
+  std::string key_src = src + "|" + kArch + "|nvrtc" + std::to_string(maj) + "." + std::to_string(minr) + "|" +
+                        std::to_string(sgmcg::fnv1a(kDevHeader)) + std::to_string(sgmcg::fnv1a(kUtilHeader));
+  char name[64];
+  snprintf(name, sizeof name, "%016" PRIx64 ".cubin", sgmcg::fnv1a(key_src));
+  std::string path = cache_dir() + "/" + name;
+  if (read_file(path, cubin)) {
+    ms = 0;
+    hit = 1;
+    return SGM_OK;
+  }
+  hit = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  nvrtcProgram prog;
+  const char* hdrs[2] = {kDevHeader, kUtilHeader};
+  const char* hnames[2] = {"sgm_dev.cuh", "sgm_util.cuh"};
+  if (nvrtcCreateProgram(&prog, src.c_str(), "sgm_kernel.cu", 2, hdrs, hnames) != NVRTC_SUCCESS)
+    return set_err(SGM_ERR_NVRTC, "nvrtcCreateProgram failed");
+  const char* opts[] = {kArch, "-std=c++17", "-lineinfo", "-DNDEBUG", "--extra-device-vectorization"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t ls = 0;
+    nvrtcGetProgramLogSize(prog, &ls);
+    std::string log(ls, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    if (log.size() > 1800) log = log.substr(0, 1800);
+    return set_err(SGM_ERR_NVRTC, "NVRTC: %s\n%s", nvrtcGetErrorString(r), log.c_str());
+  }
+  size_t cs = 0;
+  nvrtcGetCUBINSize(prog, &cs);
+  cubin.assign(cs, '\0');
+  nvrtcGetCUBIN(prog, &cubin[0]);
+  nvrtcDestroyProgram(&prog);
+  ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  write_file_atomic(path, cubin);
+  return SGM_OK;
+}
+
+int ensure_ctx() {
+  if (t_device < 0 || !g_dev[t_device].init) return set_err(SGM_ERR_NOT_INIT, "sgm_init(device) not called on this thread");
+  CU(D.cuCtxSetCurrent(g_dev[t_device].ctx));
+  return SGM_OK;
+}
+
+int launch_1d(CUfunction f, int64_t n, CUstream s, void** params) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  CU(D.cuLaunchKernel(f, (unsigned)blocks, 1, 1, 256, 1, 1, 0, s, params, nullptr));
+  return SGM_OK;
+}
+
+size_t esize(int ns) { return ns == SGM_F64 ? 8 : ns == SGM_BF16 ? 2 : 4; }
+
+}  // namespace
+
+struct sgm_plan {
+  sgmcg::GenResult gen;
+  int device = 0;
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  CUdeviceptr scratch = 0;
+  int numsys = 0;
+  int n_in = 0, n_out = 0;
+  size_t in_bytes[SGM_MAX_SLOTS] = {0};
+  size_t out_bytes[SGM_MAX_SLOTS] = {0};
+  int64_t out_elems[SGM_MAX_SLOTS] = {0};
+  double compile_ms = 0;
+  int cache_hit = 0;
+  // e2e staging
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  CUdeviceptr dev_io = 0;
+  size_t dev_io_bytes = 0;
+  CUstream tstream = nullptr;
+};
+
+extern "C" {
+
+int sgm_abi_version(void) { return SGM_ABI_VERSION; }
+const char* sgm_last_error(void) { return g_err.c_str(); }
+
+int sgm_set_cache_dir(const char* path) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache_dir = path ? path : "";
+  return SGM_OK;
+}
+
+int sgm_init(int device) {
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (device < 0 || device >= 16) return set_err(SGM_ERR_INVALID, "bad device %d", device);
+  if (!D.load()) return set_err(SGM_ERR_CUDA, "cannot load libcuda.so.1 (no NVIDIA driver on this machine)");
+  DevState& S = g_dev[device];
+  if (!S.init) {
+    CU(D.cuInit(0));
+    CU(D.cuDeviceGet(&S.dev, device));
+    CU(D.cuDevicePrimaryCtxRetain(&S.ctx, S.dev));
+    CU(D.cuCtxSetCurrent(S.ctx));
+    D.cuDeviceGetAttribute(&S.sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, S.dev);
+    D.cuDeviceGetAttribute(&S.cc_major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, S.dev);
+    D.cuDeviceGetAttribute(&S.cc_minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, S.dev);
+    if (S.cc_major != 10 || S.cc_minor != 0)
+      return set_err(SGM_ERR_CUDA, "device %d is sm_%d%d; libsgm targets sm_100a (B200) only", device, S.cc_major,
+                     S.cc_minor);
+    std::string cubin;
+    double ms;
+    int hit;
+    int st = compile_cubin("#include \"sgm_util.cuh\"\n", cubin, ms, hit);
+    if (st) return st;
+    CU(D.cuModuleLoadData(&S.util, cubin.data()));
+    CU(D.cuModuleGetFunction(&S.f_fill64, S.util, "sgm_fill64"));
+    CU(D.cuModuleGetFunction(&S.f_fill32, S.util, "sgm_fill32"));
+    CU(D.cuModuleGetFunction(&S.f_fill16, S.util, "sgm_fill16"));
+    CU(D.cuModuleGetFunction(&S.f_ff_fill, S.util, "sgm_ff_fill"));
+    CU(D.cuModuleGetFunction(&S.f_cmp, S.util, "sgm_cmp_u32"));
+    CU(D.cuModuleGetFunction(&S.f_re64, S.util, "sgm_relerr_f64"));
+    CU(D.cuModuleGetFunction(&S.f_re32, S.util, "sgm_relerr_f32"));
+    CU(D.cuModuleGetFunction(&S.f_re16, S.util, "sgm_relerr_bf16"));
+    CU(D.cuModuleGetFunction(&S.f_n64, S.util, "sgm_normal_f64"));
+    CU(D.cuModuleGetFunction(&S.f_n32, S.util, "sgm_normal_f32"));
+    CU(D.cuModuleGetFunction(&S.f_n16, S.util, "sgm_normal_bf16"));
+    CU(D.cuMemAlloc(&S.red, 64));
+    S.init = true;
+  }
+  t_device = device;
+  CU(D.cuCtxSetCurrent(S.ctx));
+  return SGM_OK;
+}
+
+int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
+  if (!desc || !out) return set_err(SGM_ERR_INVALID, "null argument");
+  *out = nullptr;
+  int sms = (t_device >= 0 && g_dev[t_device].init) ? g_dev[t_device].sms : 148;
+  sgmcg::GenResult gr = sgmcg::generate(*desc, sms);
+  if (gr.status != SGM_OK) return set_err(gr.status, "%s", gr.error.c_str());
+  sgm_plan* p = new sgm_plan();
+  p->gen = gr;
+  p->numsys = desc->numsys;
+  p->n_in = desc->n_inputs;
+  p->n_out = desc->n_outputs;
+  for (int k = 0; k < desc->n_inputs; ++k) {
+    int64_t n = 1;
+    for (int j = 0; j < desc->inputs[k].rank; ++j) n *= desc->inputs[k].dims[j];
+    p->in_bytes[k] = (size_t)n * esize(desc->numsys);
+  }
+  for (int k = 0; k < desc->n_outputs; ++k) {
+    int64_t n = 1;
+    for (int j = 0; j < desc->outputs[k].rank; ++j) n *= desc->outputs[k].dims[j];
+    p->out_elems[k] = n;
+    p->out_bytes[k] = (size_t)n * esize(desc->numsys);
+  }
+  std::string cubin;
+  int st = compile_cubin(gr.source, cubin, p->compile_ms, p->cache_hit);
+  if (st) {
+    delete p;
+    return st;
+  }
+  if (t_device < 0) {  // compile-only use (no device bound): keep the source, no module
+    *out = p;
+    return SGM_OK;
+  }
+  p->device = t_device;
+  if ((st = ensure_ctx())) { delete p; return st; }
+  CUresult r = D.cuModuleLoadData(&p->mod, cubin.data());
+  if (r != CUDA_SUCCESS) { delete p; return cu_check(r, "cuModuleLoadData"); }
+  r = D.cuModuleGetFunction(&p->fn, p->mod, gr.kernel_name.c_str());
+  if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuModuleGetFunction"); }
+  if (gr.smem_bytes > 48 * 1024) {
+    r = D.cuFuncSetAttribute(p->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, gr.smem_bytes);
+    if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuFuncSetAttribute(smem)"); }
+  }
+  if (gr.cluster > 8) {
+    r = D.cuFuncSetAttribute(p->fn, CU_FUNC_ATTRIBUTE_NON_PORTABLE_CLUSTER_SIZE_ALLOWED, 1);
+    if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuFuncSetAttribute(cluster)"); }
+  }
+  if (gr.scratch_bytes > 0) {
+    r = D.cuMemAlloc(&p->scratch, (size_t)gr.scratch_bytes);
+    if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuMemAlloc(scratch)"); }
+  }
+  *out = p;
+  return SGM_OK;
+}
+
+int sgm_plan_info_get(const sgm_plan* p, sgm_plan_info* info) {
+  if (!p || !info) return set_err(SGM_ERR_INVALID, "null argument");
+  memset(info, 0, sizeof *info);
+  info->logical_blocks = p->gen.logical_blocks;
+  info->ctas = p->gen.ctas;
+  info->cluster = p->gen.cluster;
+  info->threads = p->gen.threads;
+  info->smem_bytes = p->gen.smem_bytes;
+  info->loop_parts = p->gen.loop_parts;
+  info->free_parts = p->gen.free_parts;
+  info->scratch_bytes = p->gen.scratch_bytes;
+  info->compile_ms = p->compile_ms;
+  info->cache_hit = p->cache_hit;
+  info->n_tcgen05 = p->gen.n_tcgen05;
+  info->source_hash = sgmcg::fnv1a(p->gen.source);
+  snprintf(info->kernel_name, sizeof info->kernel_name, "%s", p->gen.kernel_name.c_str());
+  snprintf(info->plan_summary, sizeof info->plan_summary, "%s", p->gen.summary.c_str());
+  return SGM_OK;
+}
+
+int sgm_plan_source(const sgm_plan* p, char* buf, size_t cap, size_t* len) {
+  if (!p) return set_err(SGM_ERR_INVALID, "null plan");
+  if (len) *len = p->gen.source.size();
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, p->gen.source.size());
+    memcpy(buf, p->gen.source.data(), n);
+    buf[n] = 0;
+  }
+  return SGM_OK;
+}
+
+int sgm_plan_destroy(sgm_plan* p) {
+  if (!p) return SGM_OK;
+  if (p->mod || p->scratch || p->pinned || p->dev_io || p->tstream) {
+    if (D.ok && p->device >= 0 && g_dev[p->device].init) D.cuCtxSetCurrent(g_dev[p->device].ctx);
+    if (p->mod) D.cuModuleUnload(p->mod);
+    if (p->scratch) D.cuMemFree(p->scratch);
+    if (p->dev_io) D.cuMemFree(p->dev_io);
+    if (p->pinned) D.cuMemFreeHost(p->pinned);
+    if (p->tstream) D.cuStreamDestroy(p->tstream);
+  }
+  delete p;
+  return SGM_OK;
+}
+
+static int fill_nan(int ns, CUdeviceptr p, int64_t n, CUstream s) {
+  DevState& S = g_dev[t_device];
+  if (ns == SGM_F64) {
+    uint64_t v = 0x7ff8000000000000ull;
+    void* a[] = {&p, &n, &v};
+    return launch_1d(S.f_fill64, n, s, a);
+  } else if (ns == SGM_BF16) {
+    uint16_t v = 0x7fc0;
+    void* a[] = {&p, &n, &v};
+    return launch_1d(S.f_fill16, n, s, a);
+  }
+  uint32_t v = ns == SGM_FF ? 0xFFFFFFFFu : 0x7fc00000u;
+  void* a[] = {&p, &n, &v};
+  return launch_1d(S.f_fill32, n, s, a);
+}
+
+static int launch_plan(sgm_plan* p, const void* const* inputs, void* const* outputs, CUstream s) {
+  sgm::Args args;
+  memset(&args, 0, sizeof args);
+  for (int k = 0; k < p->n_in; ++k) args.in[k] = inputs[k];
+  for (int k = 0; k < p->n_out; ++k) args.out[k] = outputs[k];
+  args.scratch = (void*)p->scratch;
+  void* params[] = {&args};
+  CU(D.cuLaunchKernel(p->fn, (unsigned)p->gen.ctas, 1, 1, (unsigned)p->gen.threads, 1, 1,
+                      (unsigned)p->gen.smem_bytes, s, params, nullptr));
+  return SGM_OK;
+}
+
+int sgm_plan_run(sgm_plan* p, const void* const* inputs, void* const* outputs, int init_outputs, void* stream) {
+  if (!p) return set_err(SGM_ERR_INVALID, "null plan");
+  if (!p->fn) return set_err(SGM_ERR_NOT_INIT, "plan was created without a device (call sgm_init first)");
+  int st = ensure_ctx();
+  if (st) return st;
+  CUstream s = (CUstream)stream;
+  if (init_outputs)
+    for (int k = 0; k < p->n_out; ++k)
+      if ((st = fill_nan(p->numsys, (CUdeviceptr)outputs[k], p->out_elems[k], s))) return st;
+  return launch_plan(p, inputs, outputs, s);
+}
+
+int sgm_plan_run_host(sgm_plan* p, const void* const* host_inputs, void* const* host_outputs, void* stream) {
+  if (!p || !p->fn) return set_err(SGM_ERR_INVALID, "null plan / no device");
+  int st = ensure_ctx();
+  if (st) return st;
+  size_t tot = 0;
+  for (int k = 0; k < p->n_in; ++k) tot += (p->in_bytes[k] + 255) / 256 * 256;
+  for (int k = 0; k < p->n_out; ++k) tot += (p->out_bytes[k] + 255) / 256 * 256;
+  if (tot > p->pinned_bytes) {
+    if (p->pinned) D.cuMemFreeHost(p->pinned);
+    if (p->dev_io) D.cuMemFree(p->dev_io);
+    p->pinned = nullptr;
+    p->dev_io = 0;
+    CU(D.cuMemHostAlloc(&p->pinned, tot, 0));
+    CU(D.cuMemAlloc(&p->dev_io, tot));
+    p->pinned_bytes = p->dev_io_bytes = tot;
+  }
+  CUstream s = (CUstream)stream;
+  const void* din[SGM_MAX_SLOTS];
+  void* dout[SGM_MAX_SLOTS];
+  size_t off = 0;
+  for (int k = 0; k < p->n_in; ++k) {
+    memcpy((char*)p->pinned + off, host_inputs[k], p->in_bytes[k]);
+    CU(D.cuMemcpyHtoDAsync(p->dev_io + off, (char*)p->pinned + off, p->in_bytes[k], s));
+    din[k] = (const void*)(p->dev_io + off);
+    off += (p->in_bytes[k] + 255) / 256 * 256;
+  }
+  size_t out0 = off;
+  for (int k = 0; k < p->n_out; ++k) {
+    dout[k] = (void*)(p->dev_io + off);
+    if ((st = fill_nan(p->numsys, (CUdeviceptr)dout[k], p->out_elems[k], s))) return st;
+    off += (p->out_bytes[k] + 255) / 256 * 256;
+  }
+  if ((st = launch_plan(p, din, dout, s))) return st;
+  off = out0;
+  for (int k = 0; k < p->n_out; ++k) {
+    CU(D.cuMemcpyDtoHAsync((char*)p->pinned + off, (CUdeviceptr)dout[k], p->out_bytes[k], s));
+    off += (p->out_bytes[k] + 255) / 256 * 256;
+  }
+  CU(D.cuStreamSynchronize(s));
+  off = out0;
+  for (int k = 0; k < p->n_out; ++k) {
+    memcpy(host_outputs[k], (char*)p->pinned + off, p->out_bytes[k]);
+    off += (p->out_bytes[k] + 255) / 256 * 256;
+  }
+  return SGM_OK;
+}
+
+int sgm_plan_time(sgm_plan* p, const void* const* inputs, void* const* outputs, int rot, int warmup, int iters,
+                  void* stream, double* mean_us) {
+  if (!p || !p->fn || !mean_us) return set_err(SGM_ERR_INVALID, "null plan / no device");
+  int st = ensure_ctx();
+  if (st) return st;
+  if (rot < 1) rot = 1;
+  if (iters < 1) iters = 1;
+  if (!p->tstream) CU(D.cuStreamCreate(&p->tstream, CU_STREAM_NON_BLOCKING));
+  CUstream s = p->tstream;
+  CUstream user = (CUstream)stream;
+  if (user) CU(D.cuStreamSynchronize(user));
+  for (int w = 0; w < warmup; ++w)
+    if ((st = launch_plan(p, inputs + (size_t)(w % rot) * p->n_in, outputs, s))) return st;
+  // capture `iters` launches into one graph (launch overhead off the critical path)
+  CUgraph g = nullptr;
+  CUgraphExec ge = nullptr;
+  bool graph_ok = D.cuStreamBeginCapture(s, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL) == CUDA_SUCCESS;
+  if (graph_ok) {
+    for (int i = 0; i < iters; ++i) {
+      if (launch_plan(p, inputs + (size_t)(i % rot) * p->n_in, outputs, s)) { graph_ok = false; break; }
+    }
+    CUresult r = D.cuStreamEndCapture(s, &g);
+    graph_ok = graph_ok && r == CUDA_SUCCESS && g;
+    if (graph_ok) graph_ok = D.cuGraphInstantiateWithFlags(&ge, g, 0) == CUDA_SUCCESS;
+  }
+  CUevent e0, e1;
+  CU(D.cuEventCreate(&e0, 0));
+  CU(D.cuEventCreate(&e1, 0));
+  if (graph_ok) CU(D.cuGraphLaunch(ge, s));  // warm the graph once
+  CU(D.cuStreamSynchronize(s));
+  CU(D.cuEventRecord(e0, s));
+  if (graph_ok) {
+    CU(D.cuGraphLaunch(ge, s));
+  } else {
+    for (int i = 0; i < iters; ++i)
+      if ((st = launch_plan(p, inputs + (size_t)(i % rot) * p->n_in, outputs, s))) return st;
+  }
+  CU(D.cuEventRecord(e1, s));
+  CU(D.cuEventSynchronize(e1));
+  float ms = 0;
+  CU(D.cuEventElapsedTime(&ms, e0, e1));
+  *mean_us = (double)ms * 1000.0 / iters;
+  D.cuEventDestroy(e0);
+  D.cuEventDestroy(e1);
+  if (ge) D.cuGraphExecDestroy(ge);
+  if (g) D.cuGraphDestroy(g);
+  return SGM_OK;
+}
+
+int sgm_ff_fill(uint32_t* dst, int64_t n, uint64_t seed, uint64_t salt, void* stream) {
+  int st = ensure_ctx();
+  if (st) return st;
+  auto mix = [](uint64_t z) {
+    z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ULL;
+    z ^= z >> 27; z *= 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return z;
+  };
+  uint64_t key = mix(seed ^ mix(salt));
+  CUdeviceptr p = (CUdeviceptr)dst;
+  void* a[] = {&p, &n, &key};
+  return launch_1d(g_dev[t_device].f_ff_fill, n, (CUstream)stream, a);
+}
+
+int sgm_compare_u32(const uint32_t* a, const uint32_t* b, int64_t n, void* stream, int64_t* mismatches) {
+  int st = ensure_ctx();
+  if (st) return st;
+  DevState& S = g_dev[t_device];
+  CUstream s = (CUstream)stream;
+  CU(D.cuMemsetD32Async(S.red, 0, 16, s));
+  CUdeviceptr pa = (CUdeviceptr)a, pb = (CUdeviceptr)b;
+  void* args[] = {&pa, &pb, &n, &S.red};
+  if ((st = launch_1d(S.f_cmp, n, s, args))) return st;
+  uint64_t c = 0;
+  CU(D.cuMemcpyDtoHAsync(&c, S.red, 8, s));
+  CU(D.cuStreamSynchronize(s));
+  *mismatches = (int64_t)c;
+  return SGM_OK;
+}
+
+int sgm_rel_err(const void* a, const void* b, int64_t n, int numsys, void* stream, double* out) {
+  int st = ensure_ctx();
+  if (st) return st;
+  DevState& S = g_dev[t_device];
+  CUstream s = (CUstream)stream;
+  CU(D.cuMemsetD32Async(S.red, 0, 16, s));
+  CUdeviceptr pa = (CUdeviceptr)a, pb = (CUdeviceptr)b;
+  void* args[] = {&pa, &pb, &n, &S.red};
+  CUfunction f = numsys == SGM_F64 ? S.f_re64 : numsys == SGM_BF16 ? S.f_re16 : S.f_re32;
+  if (numsys == SGM_FF) return set_err(SGM_ERR_INVALID, "rel_err is undefined for finite-field buffers");
+  if ((st = launch_1d(f, n, s, args))) return st;
+  uint64_t r[3] = {0, 0, 0};
+  CU(D.cuMemcpyDtoHAsync(r, S.red, 24, s));
+  CU(D.cuStreamSynchronize(s));
+  double md, mb;
+  memcpy(&md, &r[0], 8);
+  memcpy(&mb, &r[1], 8);
+  *out = r[2] ? INFINITY : md / (1.0 + mb);
+  return SGM_OK;
+}
+
+int sgm_fill_normal(void* dst, int64_t n, int numsys, uint64_t seed, void* stream) {
+  int st = ensure_ctx();
+  if (st) return st;
+  DevState& S = g_dev[t_device];
+  CUdeviceptr p = (CUdeviceptr)dst;
+  void* a[] = {&p, &n, &seed};
+  CUfunction f = numsys == SGM_F64 ? S.f_n64 : numsys == SGM_BF16 ? S.f_n16 : S.f_n32;
+  if (numsys == SGM_FF) return sgm_ff_fill((uint32_t*)dst, n, seed, 0, stream);
+  return launch_1d(f, n, (CUstream)stream, a);
+}
+
+}  // extern "C"

@@ -1,0 +1,208 @@
+"""Launch-size tuning with the B200 profiler as the scoring backend.
+
+  enumerate_param_space(graph, mapping, budget_bytes)   tuner.py:74-106
+  smem_usage(graph, mapping, params)                     tuner.py:67-71
+  cost_stats / score_cost / CostModel                    tuner.py:113-157
+  score_b200(concrete, trials=3, seed=0)                 replaces score_interp (tuner.py:160-174)
+  tune(graph, mapping, backend="cost", ...)              tuner.py:188-224, plus backend="b200"
+
+score_b200 returns seconds per launch like score_interp, measured with CUDA
+events around a CUDA graph of back-to-back launches on device-resident inputs
+rotated so that each launch misses L2.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from itertools import product
+from math import prod
+from typing import Optional
+
+import numpy as np
+
+from . import _abi, ir
+from .errors import EmptyParamSpaceError, NonIntegerError
+from .plan import PLANS, numsys_of, torch, torch_dtype
+
+DEFAULT_BUDGET = 164 * 1024
+ELEMENT_BYTES = 2
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _cand(graph, mapping=None, params=None) -> ir.Candidate:
+    return ir.candidate_of(graph, mapping, params)
+
+
+def _active_extents(c: ir.Candidate, pname: str) -> list:
+    out = []
+    for n in c.block.nodes:
+        if n.kind == ir.INPUT:
+            var = n.tensor
+        elif n.kind == ir.OUTPUT:
+            var = c.program.saver_var(n.tensor)
+        else:
+            continue
+        for d, size in enumerate(c.program.spec(n.tensor).dims):
+            if size > 1 and c.on(var, d, pname):
+                out.append(size)
+    return out
+
+
+def smem_usage(graph, mapping=None, params=None) -> int:
+    c = _cand(graph, mapping, params)
+    return sum(prod(s) for s in ir.concrete_shapes(c).values()) * ELEMENT_BYTES
+
+
+def enumerate_param_space(graph, mapping=None, budget_bytes: Optional[int] = DEFAULT_BUDGET) -> list:
+    """Power-of-two sizes per parallel dim up to the smallest extent it splits
+    (1 if it splits nothing), kept if divisible and within the budget; in
+    lexicographic order over (grid dims..., loop)."""
+    c = _cand(graph, mapping)
+    names = list(c.block.pdims)
+    axes = []
+    for q in names:
+        ext = _active_extents(c, q)
+        if not ext:
+            axes.append([1])
+            continue
+        axes.append([1 << k for k in range(int(math.log2(min(ext))) + 1) if (1 << k) <= min(ext)])
+    space = []
+    for combo in product(*axes):
+        params = dict(zip(names, combo))
+        try:
+            usage = smem_usage(c.with_params(params))
+        except NonIntegerError:
+            continue
+        if budget_bytes is None or usage <= budget_bytes:
+            space.append(params)
+    return space
+
+
+@dataclass(frozen=True)
+class CostModel:
+    alpha: float = 1.0
+    beta: float = 1.0
+
+
+def cost_stats(concrete) -> dict:
+    c = _cand(concrete)
+    shapes = ir.concrete_shapes(c)
+    blocks = prod(c.params[q] for q in c.block.grid)
+    n_loop = c.params[c.block.loop]
+    body = c.block.body()
+    loaded = stored = flops = 0.0
+    for n in c.block.nodes:
+        tile = prod(shapes[n.idx])
+        reps = blocks * (n_loop if n.idx in body else 1)
+        if n.kind == ir.INPUT:
+            loaded += tile * ELEMENT_BYTES * reps
+        elif n.kind == ir.OUTPUT:
+            stored += tile * ELEMENT_BYTES * blocks
+        elif n.kind == ir.MATMUL:
+            flops += 2.0 * tile * shapes[n.inputs[0]][-1] * reps
+        else:
+            flops += tile * reps
+    return {"bytes_loaded": loaded, "bytes_stored": stored, "flops": flops, "block_count": float(blocks)}
+
+
+def score_cost(concrete, model: CostModel = CostModel()) -> float:
+    s = cost_stats(concrete)
+    return model.alpha * (s["bytes_loaded"] + s["bytes_stored"]) + model.beta * s["flops"] / s["block_count"]
+
+
+class Workspace:
+    """Device-resident rotating input sets + outputs for timing one program."""
+
+    def __init__(self, program: ir.Program, numsys: int, device: int, seed: int = 0, min_rot_bytes: int = 3 * L2_BYTES,
+                 max_rot: int = 16):
+        t = torch()
+        self.numsys = numsys
+        self.device = device
+        es = {_abi.F64: 8, _abi.F32: 4, _abi.BF16: 2, _abi.FF: 4}[numsys]
+        set_bytes = sum(prod(program.spec(n).dims) for n in program.inputs) * es
+        self.rot = max(1, min(max_rot, math.ceil(min_rot_bytes / max(set_bytes, 1))))
+        import ctypes as C
+        L = _abi.lib()
+        _abi.bind_device(device)
+        s = C.c_void_p(t.cuda.current_stream(device).cuda_stream)
+        self.sets = []
+        for r in range(self.rot):
+            cur = []
+            for k, n in enumerate(program.inputs):
+                x = t.empty(tuple(program.spec(n).dims), dtype=torch_dtype(numsys), device=device)
+                _abi.check(L.sgm_fill_normal(C.c_void_p(x.data_ptr()), x.numel(), numsys,
+                                             (seed * 1000003 + r * 131 + k) & ((1 << 64) - 1), s))
+                cur.append(x)
+            self.sets.append(cur)
+        self.outputs = [t.empty(tuple(program.spec(n).dims), dtype=torch_dtype(numsys), device=device)
+                        for n in program.outputs]
+        self.set_bytes = set_bytes
+
+
+_WORKSPACES: dict = {}
+
+
+def workspace(program: ir.Program, numsys: int, device: int) -> Workspace:
+    key = (repr(program.to_json()), numsys, device)
+    ws = _WORKSPACES.get(key)
+    if ws is None:
+        ws = _WORKSPACES[key] = Workspace(program, numsys, device)
+    return ws
+
+
+def score_b200(concrete, trials: int = 3, seed: int = 0, *, dtype=np.float32, device: Optional[int] = None,
+               iters: int = 50, warmup: int = 3, hints: Optional[dict] = None) -> float:
+    """Seconds per launch of the generated kernel (median over `trials`
+    measurements of `iters` back-to-back launches)."""
+    from .interp import device_index
+    c = _cand(concrete)
+    ns = numsys_of(dtype)
+    dev = device_index(device)
+    ws = workspace(c.program, ns, dev)
+    plan = PLANS.get(c, ns, hints, dev)
+    us = sorted(plan.time(ws.sets, ws.outputs, warmup=warmup, iters=iters) for _ in range(max(trials, 1)))
+    return us[len(us) // 2] * 1e-6
+
+
+@dataclass
+class ProfileResult:
+    params: dict
+    score: float
+    equivalence_checked: bool = False
+
+
+def tune(graph, mapping, backend: str = "cost", samples: int = 16, seed: int = 0,
+         budget_bytes: Optional[int] = DEFAULT_BUDGET, trials: int = 3, model: CostModel = CostModel(), *,
+         dtype=np.float32, device: Optional[int] = None) -> ProfileResult:
+    """tuner.py:188-224 with backend "b200" (GPU profiler) added."""
+    c = _cand(graph, mapping)
+    space = enumerate_param_space(c, budget_bytes=budget_bytes)
+    if not space:
+        raise EmptyParamSpaceError(c.program.name)
+    names = list(c.block.pdims)
+    space.sort(key=lambda d: tuple(d[n] for n in names))
+    rng = np.random.default_rng(seed)
+    if samples < len(space):
+        picked = sorted(rng.choice(len(space), size=samples, replace=False).tolist())
+        points = [space[i] for i in picked]
+    else:
+        points = space
+    best = None
+    for params in points:
+        cc = c.with_params(params)
+        if backend == "cost":
+            ir.validate(cc, strict_mapping=False)
+            score = score_cost(cc, model)
+        elif backend == "b200":
+            ir.validate(cc, strict_mapping=False)
+            score = score_b200(cc, trials=trials, seed=seed, dtype=dtype, device=device)
+        elif backend == "interp":
+            from symfuse.tuner import score_interp  # CPU reference; needs the reference install
+            from symfuse.graph import instantiate
+            score = score_interp(instantiate(graph, mapping, params), trials=trials, seed=seed)
+        else:
+            raise ValueError(f"unknown backend {backend!r}")
+        key = (score, tuple(params[n] for n in names))
+        if best is None or key < best[0]:
+            best = (key, params)
+    return ProfileResult(params=best[1], score=best[0][0])
