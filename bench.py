@@ -1,0 +1,366 @@
+"""Benchmark: candidate evaluation throughput of the five-workload SIGMA
+population on N B200s, plus best-kernel latency vs the HBM roofline.
+
+A *step* is one pass of the hot path over the full population (BASELINE
+config 5: every verified (template, mapping) x divisibility-only params of
+R, G(14336), A, Q, L): per candidate a finite-field equivalence check against
+the program and a CUDA-event timing of the generated kernel in the deployment
+dtype, then the per-workload argmin (one NCCL all_reduce(MIN) per workload).
+Candidates are sharded over ranks (LPT), so `scaling` is "strong".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the reference's CPU path (the oracle port of
+symfuse interp.run_concrete / run_program, numpy fp64) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidates evaluated/sec (five-workload population; FF check + CUDA-event profile per candidate)"
+FALLBACK_HBM = 6650.0
+
+
+def peaks() -> tuple:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 0)), "measured"
+    except Exception:
+        return FALLBACK_HBM, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for k, n in enumerate(names):
+                if len(s) > 3 + k and s[3 + k] == "Active":
+                    reasons.add(n)
+        loaded = [v for v in sm if v > 300] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU arm
+
+
+def cpu_eval_sample(seconds: float, workloads, seed: int = 0) -> dict:
+    """The reference's CPU candidate evaluation (oracle port of interp.run_concrete /
+    run_program, numpy fp64) on a bounded sample of the population:
+    per candidate one timed run_concrete (score_interp) + one equivalence trial."""
+    import numpy as np
+
+    from oracle import block_np
+    from paper_2604_15272_b200 import ir
+    from paper_2604_15272_b200 import population as P
+
+    pops = {w: P.load_population(w) for w in workloads}
+    order = []
+    per = {w: P.units(pops[w]) for w in workloads}
+    k = 0
+    while any(per.values()) and k < 10000:
+        for w in workloads:
+            if per[w]:
+                order.append(per[w].pop(len(per[w]) // 2 if k % 2 else 0))
+        k += 1
+    rng = np.random.default_rng(seed)
+    inputs = {}
+    t0 = time.perf_counter()
+    done = 0
+    for u in order:
+        if time.perf_counter() - t0 > seconds and done:
+            break
+        pop = pops[u.workload]
+        prog = pop["program"]
+        if u.workload not in inputs:
+            inputs[u.workload] = {t["name"]: rng.standard_normal(tuple(t["dims"])) for t in prog["tensors"]
+                                  if t["role"] == "input"}
+        ins = inputs[u.workload]
+        key = ir.template_key(u.cand)
+        block_np.run_concrete(prog, key, u.cand.params, ins)          # score_interp run
+        got = block_np.run_concrete(prog, key, u.cand.params, ins)    # equivalence trial
+        exp = block_np.run_program(prog, ins)
+        max(block_np.rel_err(got[n], exp[n]) for n in prog["outputs"])
+        done += 1
+    el = time.perf_counter() - t0
+    return {"candidates": done, "seconds": el, "value": done / el,
+            "sample": f"{done} candidates round-robin over {','.join(workloads)} (fp64 numpy, full scale)"}
+
+
+def reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    workloads = args.workloads
+    per_step = max(3.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_eval_sample(per_step, workloads)
+    vals, cands, secs = [], 0, 0.0
+    for _ in range(args.steps):
+        r = cpu_eval_sample(per_step, workloads)
+        cands += r["candidates"]
+        secs += r["seconds"]
+        sample = r["sample"]
+    v = cands / secs
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1000,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "five-workload SIGMA population (R,G,A,Q,L)",
+                                            "path": "oracle port of symfuse interp (CPU)"},
+            "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference", "ours"])
+    ap.add_argument("--workloads", default="R,G,A,Q,L")
+    ap.add_argument("--budget-us", type=float, default=1000.0, help="timing budget per candidate")
+    ap.add_argument("--best-iters", type=int, default=1000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--records", default=None, help="write all records (JSON) here (rank 0)")
+    args = ap.parse_args()
+    args.workloads = [w for w in args.workloads.split(",") if w]
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import numpy as np
+    import torch
+
+    from paper_2604_15272_b200 import _abi, ir
+    from paper_2604_15272_b200 import population as P
+    from paper_2604_15272_b200.plan import PLANS, numsys_of
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    _abi.bind_device(local)
+
+    pops = {w: P.load_population(w) for w in args.workloads}
+    all_units = [u for w in args.workloads for u in P.units(pops[w])]
+    mine = P.shard(all_units, rank, world)
+    t_c = time.perf_counter()
+    by_w = {}
+    for u in mine:
+        by_w.setdefault(u.workload, []).append(u.cand)
+    for w, cs in by_w.items():
+        P.precompile(cs, [numsys_of(pops[w]["dtype"]), _abi.FF], local)
+    compile_s = time.perf_counter() - t_c
+    ctx = {w: P.WorkloadContext(pops[w], local) for w in args.workloads}
+
+    def step():
+        recs = [P.evaluate_unit(ctx[u.workload], u, budget_us=args.budget_us) for u in mine]
+        winners = {}
+        for w in args.workloads:
+            best = P.argmin([r for r in recs if r.workload == w])
+            winners[w] = P.reduce_best(best, dist)
+        return recs, winners
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = _abi.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            recs, winners = step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = _abi.launch_count() - launches0
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_total = len(all_units)
+    value = n_total * args.steps / (ms / 1000.0)
+
+    # gather records on rank 0
+    all_recs = recs
+    if dist is not None:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, [r.__dict__ for r in recs])
+        all_recs = [P.Record(**d) for part in gathered for d in part]
+
+    # ---- e2e: the same pass through the host-buffer C-ABI (H2D/D2H inside) ----
+    e2e = None
+    if not args.no_e2e:
+        host_ff = {w: [x.cpu().numpy() for x in ctx[w].ff_inputs] for w in args.workloads}
+        host_exp = {w: [x.cpu().numpy() for x in ctx[w].ff_expected] for w in args.workloads}
+        h2d = d2h = 0
+
+        def e2e_step():
+            nonlocal h2d, d2h
+            h2d = d2h = 0
+            for u in mine:
+                c = ctx[u.workload]
+                plan = PLANS.get(u.cand, _abi.FF, None, local)
+                outs = [np.empty(tuple(c.program.spec(n).dims), dtype=np.int32) for n in c.program.outputs]
+                plan.run_host(host_ff[u.workload], outs)
+                h2d += sum(a.nbytes for a in host_ff[u.workload])
+                d2h += sum(a.nbytes for a in outs)
+                all(np.array_equal(a, b) for a, b in zip(outs, host_exp[u.workload]))
+                lat = PLANS.get(u.cand, c.numsys, None, local).time(c.ws.sets, c.ws.outputs, warmup=1, iters=5)
+                d2h += 8
+                del lat
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        e2e_step()
+        f1.record()
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if dist is not None:
+            t = torch.tensor([ems, h2d, d2h], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t[0].item())
+            h2d, d2h = int(t[1].item()) * world, int(t[2].item()) * world
+        e2e = {"value": n_total / (ems / 1000.0), "unit": "candidates/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "path": "sgm_plan_run_host (FF check with host numpy buffers) + sgm_plan_time per candidate"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- best kernels: re-time each workload's winner with the paper's 1000-run protocol ----
+    hbm, bf16_tf, peak_kind = peaks()
+    best = {}
+    for w in args.workloads:
+        wrecs = [r for r in all_recs if r.workload == w]
+        win = P.argmin(wrecs)
+        if win is None:
+            best[w] = {"error": "no valid candidate"}
+            continue
+        u = next(x for x in P.units(pops[w]) if x.index == win.index)
+        plan = PLANS.get(u.cand, ctx[w].numsys, None, local)
+        lat = plan.time(ctx[w].ws.sets, ctx[w].ws.outputs, warmup=10, iters=args.best_iters)
+        byts = P.algorithmic_bytes(pops[w])
+        gbs = byts / (lat * 1e-6) / 1e9
+        best[w] = {"latency_us": lat, "algorithmic_bytes": byts, "achieved_gbs": gbs, "frac_hbm": gbs / hbm,
+                   "template": pops[w]["candidates"][u.pair]["template_id"], "mapping": u.cand.mapping_list(),
+                   "params": u.cand.params, "kernel": plan.kernel_name, "plan": plan.info["summary"],
+                   "ctas": plan.info["ctas"], "cluster": plan.info["cluster"],
+                   "ff_ok": win.ff_ok, "candidates": len(wrecs),
+                   "failed": sum(1 for r in wrecs if r.error), "ff_mismatch": sum(1 for r in wrecs if r.ff_ok is False)}
+    head = "G" if "G" in best and "latency_us" in best["G"] else next(
+        (w for w in args.workloads if "latency_us" in best.get(w, {})), None)
+    roof = None
+    if head:
+        b = best[head]
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                traffic = json.load(fh).get(head)
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "achieved": b["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": b["achieved_gbs"] / hbm, "traffic": traffic, "kernel": b["kernel"], "workload": head,
+                "peak_kind": peak_kind}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        l0 = _abi.launch_count()
+        r = cpu_eval_sample(20.0, args.workloads)
+        assert _abi.launch_count() == l0
+        cpu = {"value": r["value"], "unit": "candidates/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": r["sample"]}
+    line = {
+        "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16/f32 timing + ff check", "data": "synthetic",
+        "config": {"workload": "five-workload SIGMA population: " + ",".join(args.workloads),
+                   "candidates": n_total, "per_candidate": f"FF check + profile (~{args.budget_us:.0f}us budget)",
+                   "l2": "inputs rotated over sets totalling >= 3x L2 (cold L2 per launch)",
+                   "compile_s_rank0": compile_s},
+        "roofline": roof, "best_kernels": best, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line))
+    if args.records:
+        with open(args.records, "w") as fh:
+            json.dump([r.__dict__ for r in all_recs], fh)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -159,6 +159,9 @@ typedef struct sgm_plan sgm_plan;
 
 int sgm_abi_version(void);
 const char* sgm_last_error(void);
+/* Kernel launches issued by this library so far (generated + utility kernels;
+ * graph launches count every node executed). */
+long long sgm_launch_count(void);
 
 /* Bind the calling thread to `device` (primary context) and load the driver. */
 int sgm_init(int device);

@@ -67,6 +67,7 @@ class PlanInfo(C.Structure):
 SYMBOLS = {
     "sgm_abi_version": ([], C.c_int),
     "sgm_last_error": ([], C.c_char_p),
+    "sgm_launch_count": ([], C.c_longlong),
     "sgm_init": ([C.c_int], C.c_int),
     "sgm_set_cache_dir": ([C.c_char_p], C.c_int),
     "sgm_plan_create": ([C.POINTER(PlanDesc), C.POINTER(C.c_void_p)], C.c_int),
@@ -127,3 +128,7 @@ def ptr_array(ptrs) -> "C.Array":
     for k, p in enumerate(ptrs):
         arr[k] = p
     return arr
+
+
+def launch_count() -> int:
+    return int(lib().sgm_launch_count())

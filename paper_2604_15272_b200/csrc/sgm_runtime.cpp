@@ -50,6 +50,7 @@ const char* kUtilHeader =
     ;
 
 thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
 
 int set_err(int st, const char* fmt, ...) {
   char buf[2048];
@@ -278,6 +279,7 @@ int launch_1d(CUfunction f, int64_t n, CUstream s, void** params) {
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   CU(D.cuLaunchKernel(f, (unsigned)blocks, 1, 1, 256, 1, 1, 0, s, params, nullptr));
+  g_launches++;
   return SGM_OK;
 }
 
@@ -309,6 +311,7 @@ struct sgm_plan {
 extern "C" {
 
 int sgm_abi_version(void) { return SGM_ABI_VERSION; }
+long long sgm_launch_count(void) { return g_launches.load(); }
 const char* sgm_last_error(void) { return g_err.c_str(); }
 
 int sgm_set_cache_dir(const char* path) {
@@ -482,6 +485,7 @@ static int launch_plan(sgm_plan* p, const void* const* inputs, void* const* outp
   void* params[] = {&args};
   CU(D.cuLaunchKernel(p->fn, (unsigned)p->gen.ctas, 1, 1, (unsigned)p->gen.threads, 1, 1,
                       (unsigned)p->gen.smem_bytes, s, params, nullptr));
+  g_launches++;  // during graph capture this counts the captured node once
   return SGM_OK;
 }
 
@@ -572,11 +576,12 @@ int sgm_plan_time(sgm_plan* p, const void* const* inputs, void* const* outputs, 
   CUevent e0, e1;
   CU(D.cuEventCreate(&e0, 0));
   CU(D.cuEventCreate(&e1, 0));
-  if (graph_ok) CU(D.cuGraphLaunch(ge, s));  // warm the graph once
+  if (graph_ok) { CU(D.cuGraphLaunch(ge, s)); g_launches += iters; }  // warm the graph once
   CU(D.cuStreamSynchronize(s));
   CU(D.cuEventRecord(e0, s));
   if (graph_ok) {
     CU(D.cuGraphLaunch(ge, s));
+    g_launches += iters;
   } else {
     for (int i = 0; i < iters; ++i)
       if ((st = launch_plan(p, inputs + (size_t)(i % rot) * p->n_in, outputs, s))) return st;
