@@ -211,8 +211,24 @@ def main() -> None:
     compile_s = time.perf_counter() - t_c
     ctx = {w: P.WorkloadContext(pops[w], local) for w in args.workloads}
 
+    def log(msg):
+        print(f"[rank{rank} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+    log(f"{len(mine)}/{len(all_units)} candidates on this rank; compile+load {compile_s:.1f}s")
+
     def step():
-        recs = [P.evaluate_unit(ctx[u.workload], u, budget_us=args.budget_us) for u in mine]
+        recs = []
+        t_w = {}
+        for u in mine:
+            t0 = time.perf_counter()
+            recs.append(P.evaluate_unit(ctx[u.workload], u, budget_us=args.budget_us))
+            t_w[u.workload] = t_w.get(u.workload, 0.0) + time.perf_counter() - t0
+        errs = sum(1 for r in recs if r.error)
+        log("step " + " ".join(f"{w}:{t:.1f}s" for w, t in t_w.items()) + f" errors={errs}")
+        for r in recs:
+            if r.error:
+                log(f"  error {r.workload}#{r.index} {r.params} {r.error[:160]}")
+                break
         winners = {}
         for w in args.workloads:
             best = P.argmin([r for r in recs if r.workload == w])
@@ -225,6 +241,7 @@ def main() -> None:
 
     for _ in range(args.warmup):
         step()
+        log("warmup step done")
     torch.cuda.synchronize()
     barrier()
     launches0 = _abi.launch_count()
@@ -255,6 +272,11 @@ def main() -> None:
         dist.all_gather_object(gathered, [r.__dict__ for r in recs])
         all_recs = [P.Record(**d) for part in gathered for d in part]
 
+    if args.records and rank == 0:
+        with open(args.records, "w") as fh:
+            json.dump([r.__dict__ for r in all_recs], fh)
+    log(f"timed: {ms / args.steps:.0f} ms/step, {n_total * args.steps / (ms / 1000.0):.1f} candidates/s")
+
     # ---- e2e: the same pass through the host-buffer C-ABI (H2D/D2H inside) ----
     e2e = None
     if not args.no_e2e:
@@ -267,15 +289,20 @@ def main() -> None:
             h2d = d2h = 0
             for u in mine:
                 c = ctx[u.workload]
-                plan = PLANS.get(u.cand, _abi.FF, None, local)
+                try:
+                    plan = PLANS.get(u.cand, _abi.FF, None, local)
+                except Exception:
+                    continue
                 outs = [np.empty(tuple(c.program.spec(n).dims), dtype=np.int32) for n in c.program.outputs]
                 plan.run_host(host_ff[u.workload], outs)
                 h2d += sum(a.nbytes for a in host_ff[u.workload])
                 d2h += sum(a.nbytes for a in outs)
                 all(np.array_equal(a, b) for a, b in zip(outs, host_exp[u.workload]))
-                lat = PLANS.get(u.cand, c.numsys, None, local).time(c.ws.sets, c.ws.outputs, warmup=1, iters=5)
+                try:
+                    PLANS.get(u.cand, c.numsys, None, local).time(c.ws.sets, c.ws.outputs, warmup=1, iters=5)
+                except Exception:
+                    pass
                 d2h += 8
-                del lat
         e2e_step()
         torch.cuda.synchronize()
         barrier()
@@ -286,6 +313,7 @@ def main() -> None:
         f1.record()
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1)
+        log(f"e2e: {ems:.0f} ms/step, h2d {h2d / 1e9:.1f} GB")
         if dist is not None:
             t = torch.tensor([ems, h2d, d2h], dtype=torch.float64, device=f"cuda:{local}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -354,9 +382,6 @@ def main() -> None:
         "gpu_launches": launches,
     }
     print(json.dumps(line))
-    if args.records:
-        with open(args.records, "w") as fh:
-            json.dump([r.__dict__ for r in all_recs], fh)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

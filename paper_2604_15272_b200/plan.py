@@ -217,10 +217,20 @@ class PlanCache:
         self._d: "OrderedDict[tuple, Plan]" = OrderedDict()
         self._lock = threading.Lock()
 
+    @staticmethod
+    def cand_key(cand: Candidate) -> str:
+        k = getattr(cand, "_plan_key", None)
+        if k is None:
+            from .ir import serialize
+            k = serialize(cand) + "|" + repr(cand.program.to_json())
+            try:
+                cand._plan_key = k
+            except AttributeError:
+                pass
+        return k
+
     def get(self, cand: Candidate, numsys: int, hints: Optional[dict] = None, device: Optional[int] = 0) -> Plan:
-        from .ir import serialize
-        key = (serialize(cand), cand.program.name, repr(cand.program.to_json()), numsys,
-               tuple(sorted((hints or {}).items())), device)
+        key = (self.cand_key(cand), numsys, tuple(sorted((hints or {}).items())), device)
         with self._lock:
             p = self._d.get(key)
             if p is not None:
@@ -235,4 +245,4 @@ class PlanCache:
         return p
 
 
-PLANS = PlanCache()
+PLANS = PlanCache(capacity=8192)

@@ -109,9 +109,10 @@ def shard(us: list, rank: int, world: int) -> list:
     return mine
 
 
-def precompile(cands: list, numsys_list, device: Optional[int], threads: int = 8, hints=None) -> dict:
+def precompile(cands: list, numsys_list, device: Optional[int], threads: int = 0, hints=None) -> dict:
     """Compile (or cache-hit) plans in parallel; returns {(serialized, ns): error or None}."""
     errs = {}
+    threads = threads or min(32, os.cpu_count() or 8)
 
     def one(arg):
         c, ns = arg
