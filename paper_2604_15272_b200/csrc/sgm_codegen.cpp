@@ -89,6 +89,8 @@ struct Node {
   bool shfl = false;
   i64 red_bytes = 0;
   int red_off = 0;
+  i64 at_bytes = 0;  // k-major copy of the gemv A operand
+  int at_off = 0;
 };
 
 struct Class {
@@ -708,6 +710,7 @@ struct Gen {
       const Node& b = nodes[x.in[1]];
       x.gemv = false;
       x.red_bytes = 0;
+      x.at_bytes = 0;
       i64 M = x.sl[2], K = a.sl[3], NN = x.sl[3];
       if (b.store == ST_VIEW && a.store != ST_VIEW && M <= 16 && NN >= 1) {
         // B stride along n must be 1 (row-major view), alignment for vectors
@@ -735,13 +738,16 @@ struct Gen {
         while (items * ks * 2 <= NT && ks * 2 <= K) ks *= 2;
         x.ks = (int)ks;
         i64 per_thread = (K + ks - 1) / ks;
-        x.unr = per_thread >= 8 ? 8 : (per_thread >= 4 ? 4 : (per_thread >= 2 ? 2 : 1));
+        int umax = (M * vn * accw <= 32) ? 16 : 8;
+        x.unr = per_thread >= umax ? umax : per_thread >= 8 ? 8 : (per_thread >= 4 ? 4 : (per_thread >= 2 ? 2 : 1));
         bool nv_pow2 = (NV & (NV - 1)) == 0;
         i64 work = items * ks;
         x.shfl = nv_pow2 && ((work % NT == 0) || (work < NT && work % 32 == 0));
         i64 kin = (!x.shfl || NV >= 32) ? 1 : std::min<i64>(32 / NV, ks);
         i64 kout = ks / kin;
         if (kout > 1) x.red_bytes = kout * items * M * vn * ea;
+        i64 a0 = (a.sl[0] > 1) ? x.sl[0] : 1, a1 = (a.sl[1] > 1) ? x.sl[1] : 1;
+        x.at_bytes = a0 * a1 * K * M * ec;
       }
     }
   }
@@ -789,6 +795,15 @@ struct Gen {
         I.bytes = nodes[n].red_bytes;
         iv.push_back(I);
       }
+    int tcount_at0 = tcount;
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (nodes[n].kind == SGM_MATMUL && nodes[n].at_bytes > 0) {
+        Interval I;
+        I.id = -(1 + tcount++);
+        I.start = I.end = pos_of[n];
+        I.bytes = nodes[n].at_bytes;
+        iv.push_back(I);
+      }
     for (int p = 0; p < S; ++p)
       if (sched[p].type == Ev::FLUSH)
         for (int f : sched[p].flush) {
@@ -826,6 +841,9 @@ struct Gen {
     int t = 0;
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].kind == SGM_MATMUL && nodes[n].red_bytes > 0) nodes[n].red_off = (int)off_of[-(1 + t++)];
+    t = tcount_at0;
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (nodes[n].kind == SGM_MATMUL && nodes[n].at_bytes > 0) nodes[n].at_off = (int)off_of[-(1 + t++)];
     for (auto& fi : flush_ids) flush_tmp_off[fi.first] = (int)off_of[fi.second];
     // global scratch for tiles that did not fit
     scratch_per_cta = 0;
@@ -984,20 +1002,22 @@ struct Gen {
   }
 
   void emit_flush(const std::vector<int>& fl, int pos) {
+    // reduce-scatter (DSMEM loads into tmp) + all-gather (DSMEM stores)
     os << "    sgm::cluster_sync();\n";
     for (int f : fl) {
       const Node& x = nodes[f];
       u32 keep = (u32)(CL - 1) & ~x.pend;
-      os << "    sgm::cl_reduce<N, " << prod4(x.sl) << ", " << CL << ", " << keep << "u, NT>(" << tile_ptr(f)
+      os << "    sgm::cl_rs_phase1<N, " << prod4(x.sl) << ", " << CL << ", " << keep << "u, NT>(" << tile_ptr(f)
          << ", (C*)(sm + " << flush_tmp_off.at({pos, f}) << "), crank);\n";
     }
     os << "    sgm::cluster_sync();\n";
     for (int f : fl) {
       const Node& x = nodes[f];
-      os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) " << tile_ptr(f) << "[e] = ((const C*)(sm + "
-         << flush_tmp_off.at({pos, f}) << "))[e];\n";
+      u32 keep = (u32)(CL - 1) & ~x.pend;
+      os << "    sgm::cl_rs_phase2<N, " << prod4(x.sl) << ", " << CL << ", " << keep << "u, NT>(" << tile_ptr(f)
+         << ", (const C*)(sm + " << flush_tmp_off.at({pos, f}) << "), crank);\n";
     }
-    os << "    __syncthreads();\n";
+    os << "    sgm::cluster_sync();\n";
   }
 
   void emit_node(int n, bool in_loop) {
@@ -1092,7 +1112,7 @@ struct Gen {
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << sb[0] << "LL, " << sb[1]
              << "LL, " << sb[2] << "LL, " << x.vn << ", " << x.ks << ", " << x.unr << ", "
              << (x.shfl ? "true" : "false") << ", NT>(" << tile_ptr(n) << ", " << pa << ", " << pb << ", (A*)(sm + "
-             << x.red_off << "));\n";
+             << x.red_off << "), (C*)(sm + " << x.at_off << "));\n";
         } else {
           std::string ta = a.store == ST_VIEW ? "S" : "C";
           std::string tb = b.store == ST_VIEW ? "S" : "C";

@@ -353,24 +353,36 @@ template <int NV, int KS, bool SHFL> struct gemv_layout {
   static constexpr int KS_OUT = KS / KS_IN_WARP;
 };
 
+// A is first re-laid k-major into `at` ([A0*A1][K][M], A0/A1 = A's own batch extents)
+// so each k step reads the M values of a column with 16-byte shared loads.
 template <class N, class TB, int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3,
           i64 SB0, i64 SB1, i64 SB2, int VN, int KS, int UNR, bool SHFL, int NT>
 __device__ __forceinline__ void mm_gemv(typename N::C* __restrict__ out, const typename N::C* __restrict__ A,
-                                        const TB* __restrict__ B, typename N::A* __restrict__ red) {
+                                        const TB* __restrict__ B, typename N::A* __restrict__ red,
+                                        typename N::C* __restrict__ at) {
   typedef typename N::A Acc;
   typedef typename N::C C;
   constexpr int NV = NN / VN;
   constexpr int ITEMS = B0 * B1 * NV;
   constexpr int WORK = ITEMS * KS;
+  constexpr int A0 = SA0 ? B0 : 1, A1 = SA1 ? B1 : 1;
   typedef gemv_layout<NV, KS, SHFL> LY;
   static_assert(NN % VN == 0, "VN must divide NN");
   const int tid = threadIdx.x;
+  for (int e = tid; e < A0 * A1 * K * M; e += NT) {
+    const int m = e % M;
+    const int k = (e / M) % K;
+    const int ab = e / (M * K);
+    const int a1 = ab % A1, a0 = ab / A1;
+    at[e] = A[a0 * SA0 + a1 * SA1 + (i64)m * SA2 + (i64)k * SA3];
+  }
+  __syncthreads();
   for (int w = tid; w < WORK; w += NT) {
     const int nv = w % NV;
     const int ks = (w / NV) % KS;
     const int bi = w / (NV * KS);
     const int b1 = bi % B1, b0 = bi / B1;
-    const C* pa = A + b0 * SA0 + b1 * SA1;
+    const C* pa = at + (i64)((SA0 ? b0 : 0) * A1 + (SA1 ? b1 : 0)) * K * M;
     const TB* pb = B + b0 * SB0 + b1 * SB1 + nv * VN;
     Acc acc[M][VN];
 #pragma unroll
@@ -409,11 +421,20 @@ __device__ __forceinline__ void mm_gemv(typename N::C* __restrict__ out, const t
           C bc[VN];
 #pragma unroll
           for (int v = 0; v < VN; ++v) bc[v] = cvs<N>(bv[u][v]);
+          C av[M];
+          if constexpr ((M * sizeof(C)) % 16 == 0) {
+#pragma unroll
+            for (int q = 0; q < (int)(M * sizeof(C) / 16); ++q)
+              *reinterpret_cast<uint4*>(&av[q * (16 / sizeof(C))]) =
+                  *reinterpret_cast<const uint4*>(pa + (i64)k * M + q * (16 / sizeof(C)));
+          } else {
+#pragma unroll
+            for (int m = 0; m < M; ++m) av[m] = pa[(i64)k * M + m];
+          }
 #pragma unroll
           for (int m = 0; m < M; ++m) {
-            const C a = pa[m * SA2 + (i64)k * SA3];
 #pragma unroll
-            for (int v = 0; v < VN; ++v) N::mac(acc[m][v], a, bc[v]);
+            for (int v = 0; v < VN; ++v) N::mac(acc[m][v], av[m], bc[v]);
           }
         }
       }
@@ -462,7 +483,55 @@ __device__ __forceinline__ void mm_gemv(typename N::C* __restrict__ out, const t
 }
 
 // ---------------------------------------------------------------------------
-// Cluster all-reduce of a partial tile: tmp[e] = sum over peers r with
+// Cluster all-reduce as reduce-scatter + all-gather over DSMEM.  The peers of
+// a group are the ranks r with ((r ^ me) & KEEP) == 0.  Phase 1: each member
+// sums the chunk it owns from every member (DSMEM loads) into `tmp`; phase 2
+// (after a cluster barrier): it stores the summed chunk into every member's tile
+// (DSMEM stores).  DSMEM traffic per CTA: SZ loads + SZ stores (vs G*SZ loads).
+// Sums run in rank order so every CTA holds bit-identical values.
+
+__host__ __device__ constexpr int cpopc(u32 x) { return x ? (int)(x & 1u) + cpopc(x >> 1) : 0; }
+
+__device__ __forceinline__ int cl_pos(u32 me, u32 keep, int cl) {
+  int pos = 0;
+  for (u32 r = 0; r < (u32)cl && r < me; ++r) pos += (((r ^ me) & keep) == 0u);
+  return pos;
+}
+
+template <class N, int SZ, int CL, u32 KEEP, int NT>
+__device__ __forceinline__ void cl_rs_phase1(const typename N::C* tile, typename N::C* tmp, u32 me) {
+  typedef typename N::A Acc;
+  constexpr int G = 1 << cpopc((u32)(CL - 1) & ~KEEP);
+  constexpr int CH = (SZ + G - 1) / G;
+  const int pos = cl_pos(me, KEEP, CL);
+  const int lo = pos * CH;
+  const int hi = (lo + CH < SZ) ? lo + CH : SZ;
+  for (int e = lo + threadIdx.x; e < hi; e += NT) {
+    Acc acc = N::azero();
+#pragma unroll
+    for (u32 r = 0; r < (u32)CL; ++r)
+      if (((r ^ me) & KEEP) == 0u) N::aadd(acc, peer_ptr(tile, r)[e]);
+    tmp[e - lo] = N::fin(acc);
+  }
+}
+
+template <class N, int SZ, int CL, u32 KEEP, int NT>
+__device__ __forceinline__ void cl_rs_phase2(typename N::C* tile, const typename N::C* tmp, u32 me) {
+  constexpr int G = 1 << cpopc((u32)(CL - 1) & ~KEEP);
+  constexpr int CH = (SZ + G - 1) / G;
+  const int pos = cl_pos(me, KEEP, CL);
+  const int lo = pos * CH;
+  const int hi = (lo + CH < SZ) ? lo + CH : SZ;
+  for (int e = lo + threadIdx.x; e < hi; e += NT) {
+    const typename N::C v = tmp[e - lo];
+#pragma unroll
+    for (u32 r = 0; r < (u32)CL; ++r)
+      if (((r ^ me) & KEEP) == 0u) const_cast<typename N::C*>(peer_ptr(tile, r))[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster all-reduce of a partial tile (simple form, used for tiny tiles): tmp[e] = sum over peers r with
 // ((r ^ me) & KEEP) == 0 of tile_r[e], in rank order (identical on every CTA).
 
 template <class N, int SZ, int CL, u32 KEEP, int NT>

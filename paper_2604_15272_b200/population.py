@@ -165,6 +165,7 @@ class Record:
     latency_us: Optional[float] = None
     error: Optional[str] = None
     plan: dict = field(default_factory=dict)
+    pruned: bool = False
 
 
 class WorkloadContext:
@@ -186,10 +187,11 @@ class WorkloadContext:
             self.ff_inputs = ff_fill_inputs(self.program, seed64, device)
             self.ff_expected = ff_run(ir.program_candidate(self.program), self.ff_inputs, device)
         self.bytes = algorithmic_bytes(pop)
+        self.best_us = None  # running best latency (prunes precise timing of losers)
 
 
 def evaluate_unit(ctx: WorkloadContext, u: Unit, budget_us: float = 2000.0, max_iters: int = 200,
-                  ff: bool = True) -> Record:
+                  ff: bool = True, prune_factor: float = 4.0) -> Record:
     from .ff import ff_equal, ff_run
     rec = Record(u.workload, u.index, u.pair, dict(u.cand.params), u.cand.mapping_list())
     try:
@@ -198,8 +200,14 @@ def evaluate_unit(ctx: WorkloadContext, u: Unit, budget_us: float = 2000.0, max_
             rec.ff_ok = all(ff_equal(g, e) for g, e in zip(got, ctx.ff_expected))
         plan = PLANS.get(u.cand, ctx.numsys, None, ctx.device)
         est = plan.time(ctx.ws.sets, ctx.ws.outputs, warmup=1, iters=1)
-        iters = int(max(5, min(max_iters, budget_us / max(est, 1.0))))
-        rec.latency_us = plan.time(ctx.ws.sets, ctx.ws.outputs, warmup=2, iters=iters)
+        if ctx.best_us is not None and est > prune_factor * ctx.best_us:
+            rec.latency_us = est  # clearly not the winner: one launch is enough evidence
+            rec.pruned = True
+        else:
+            iters = int(max(5, min(max_iters, budget_us / max(est, 1.0))))
+            rec.latency_us = plan.time(ctx.ws.sets, ctx.ws.outputs, warmup=2, iters=iters)
+            if rec.ff_ok is not False and (ctx.best_us is None or rec.latency_us < ctx.best_us):
+                ctx.best_us = rec.latency_us
         rec.plan = {k: plan.info[k] for k in ("ctas", "cluster", "smem_bytes", "free_parts", "loop_parts",
                                                "kernel_name", "summary")}
     except Exception as exc:
