@@ -91,6 +91,8 @@ struct Node {
   int red_off = 0;
   i64 at_bytes = 0;  // k-major copy of the gemv A operand
   int at_off = 0;
+  bool tc = false;   // tcgen05 realisation (bf16)
+  int tc_kc = 16, tc_s = 4, tc_cols = 32;
 };
 
 struct Class {
@@ -709,6 +711,7 @@ struct Gen {
       const Node& a = nodes[x.in[0]];
       const Node& b = nodes[x.in[1]];
       x.gemv = false;
+      x.tc = false;
       x.red_bytes = 0;
       x.at_bytes = 0;
       i64 M = x.sl[2], K = a.sl[3], NN = x.sl[3];
@@ -748,6 +751,27 @@ struct Gen {
         if (kout > 1) x.red_bytes = kout * items * M * vn * ea;
         i64 a0 = (a.sl[0] > 1) ? x.sl[0] : 1, a1 = (a.sl[1] > 1) ? x.sl[1] : 1;
         x.at_bytes = a0 * a1 * K * M * ec;
+        // tcgen05 path: bf16 weights, <= 16 rows, K in multiples of 16, 16-byte row alignment
+        x.tc = false;
+        bool row16 = true;
+        for (int k = 0; k < 3; ++k)
+          if (in_dims[b.slot][k] > 1 && (in_strides[b.slot][k] * es) % 16) row16 = false;
+        i64 ntl = (NN + 127) / 128;
+        if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && NN % 8 == 0 && NN >= 64 &&
+            ntl <= 32 && row16 && x.sl[0] * x.sl[1] <= 8) {
+          i64 kc = 16;
+          while (kc * 2 <= K && K % (kc * 2) == 0 && ntl * (kc * 2 / 8) * 2048 <= 24 * 1024) kc *= 2;
+          int S = 4;
+          i64 bytes = S * ntl * (kc / 8) * 2048 + 32 * K + 8 * (S + 1);
+          x.tc = true;
+          x.tc_kc = (int)kc;
+          x.tc_s = S;
+          int cols = 32;
+          while (cols < ntl * 16) cols *= 2;
+          x.tc_cols = cols;
+          x.red_bytes = 0;
+          x.at_bytes = bytes;  // the tcgen05 work area re-uses the transient slot
+        }
       }
     }
   }
@@ -955,11 +979,13 @@ struct Gen {
     return e.str();
   }
 
-  int io_vec(const Node& x, bool loader) const {
+  // vector width for a loader (x) or a saver (x = saver node, sl = its input's slice)
+  int io_vec(const Node& x, bool loader, const i64* sl = nullptr) const {
     const i64* dims = loader ? in_dims[x.slot] : out_dims[x.slot];
     const i64* st = loader ? in_strides[x.slot] : out_strides[x.slot];
+    if (!sl) sl = x.sl;
     int v = vecw;
-    if (x.sl[3] % v) return 1;
+    if (sl[3] % v) return 1;
     for (int k = 0; k < 3; ++k)
       if (dims[k] > 1 && st[k] % v) return 1;
     return v;
@@ -1041,7 +1067,7 @@ struct Gen {
         const i64* st = out_strides[x.slot];
         os << "    if (" << saver_pred(x) << ") sgm::store_tile<N, " << src.sl[0] << ", " << src.sl[1] << ", "
            << src.sl[2] << ", " << src.sl[3] << ", " << st[0] << "LL, " << st[1] << "LL, " << st[2] << "LL, "
-           << st[3] << "LL, " << io_vec(src, false) << ", NT>((S*)a.out[" << x.slot << "] + (" << off << "), "
+           << st[3] << "LL, " << io_vec(x, false, src.sl) << ", NT>((S*)a.out[" << x.slot << "] + (" << off << "), "
            << tile_ptr(x.in[0]) << ");\n";
         return;  // no barrier needed after a global store
       }
@@ -1107,7 +1133,12 @@ struct Gen {
         };
         std::string pa = a.store == ST_VIEW ? view_ptr(a) : tile_ptr(x.in[0]);
         std::string pb = b.store == ST_VIEW ? view_ptr(b) : tile_ptr(x.in[1]);
-        if (x.gemv) {
+        if (x.gemv && x.tc) {
+          os << "    sgm::mm_gemv_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
+             << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << sb[0] << "LL, " << sb[1]
+             << "LL, " << sb[2] << "LL, " << x.tc_kc << ", " << x.tc_s << ", NT>(" << tile_ptr(n) << ", " << pa
+             << ", " << pb << ", sm + " << x.at_off << ", tmem_base);\n";
+        } else if (x.gemv) {
           os << "    sgm::mm_gemv<N, S, " << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << sb[0] << "LL, " << sb[1]
              << "LL, " << sb[2] << "LL, " << x.vn << ", " << x.ks << ", " << x.unr << ", "
@@ -1168,6 +1199,13 @@ struct Gen {
       else if (x.store == ST_GLOBAL)
         os << "  C* " << tile_ptr(n) << " = (C*)(scr + " << x.off << ");\n";
     }
+    int tmem_cols = 0;
+    for (auto& x : nodes)
+      if (x.kind == SGM_MATMUL && x.gemv && x.tc) tmem_cols = std::max(tmem_cols, x.tc_cols);
+    if (tmem_cols) {
+      os << "  __shared__ unsigned tmem_slot;\n";
+      os << "  const unsigned tmem_base = sgm::tmem_alloc(&tmem_slot, " << tmem_cols << "u);\n";
+    }
     bool in_loop = false;
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
@@ -1187,6 +1225,7 @@ struct Gen {
         emit_node(e.node, in_loop);
       }
     }
+    if (tmem_cols) os << "  sgm::tmem_free(tmem_base, " << tmem_cols << "u);\n";
     os << "}\n";
   }
 
@@ -1220,6 +1259,8 @@ struct Gen {
     R.smem_bytes = smem_peak;
     R.loop_parts = LP;
     R.scratch_bytes = scratch_per_cta * R.ctas;
+    for (auto& x : nodes)
+      if (x.kind == SGM_MATMUL && x.gemv && x.tc) R.n_tcgen05++;
     std::ostringstream s;
     s << "LB=" << LB << " FP=" << FP << " CL=" << CL << " LP=" << LP << " smem=" << smem_peak
       << " scratch/cta=" << scratch_per_cta << " classes:";
@@ -1227,7 +1268,7 @@ struct Gen {
       s << " c" << c << "(" << cls[c].extent << (cls[c].reduced ? "r" : "f") << "/" << cls[c].parts << ")";
     s << " mm:";
     for (int n = 0; n < (int)nodes.size(); ++n)
-      if (nodes[n].kind == SGM_MATMUL) s << " n" << n << (nodes[n].gemv ? "gemv" : "gen") << (nodes[n].gemv ? "/vn" + std::to_string(nodes[n].vn) + "ks" + std::to_string(nodes[n].ks) : "");
+      if (nodes[n].kind == SGM_MATMUL) s << " n" << n << (nodes[n].gemv ? (nodes[n].tc ? "tc" : "gemv") : "gen") << (nodes[n].gemv ? "/vn" + std::to_string(nodes[n].vn) + "ks" + std::to_string(nodes[n].ks) : "");
     R.summary = s.str();
     return R;
   }

@@ -483,6 +483,185 @@ __device__ __forceinline__ void mm_gemv(typename N::C* __restrict__ out, const t
 }
 
 // ---------------------------------------------------------------------------
+// tcgen05 streamed GEMV (bf16 weights, fp32 accumulate in TMEM).
+//   out[b][m][n] = sum_k A[b][m][k] * B[b][k][n],  M <= 16 (padded to the MMA N=16)
+// Swap-AB: the weight slice is the MMA A operand (M_mma = 128 output columns,
+// MN-major), A^T is the MMA B operand (N_mma = 16, K-major).  Weights stream
+// through an S-stage smem ring filled by cp.async (16-byte chunks, zero-filled
+// past NN) in the canonical no-swizzle UMMA layout:
+//   W^T core matrix = 8 k-rows x 16 B (8 n); n-groups at SBO = 128 B,
+//   k-groups at LBO = 2048 B (one 128-column tile).
+//   X^T core matrix = 8 m-rows x 16 B (8 k); m-groups at SBO = 128 B,
+//   k-groups at LBO = 256 B.
+// One thread issues the MMAs; tcgen05.commit arrives on the stage's mbarrier,
+// which gates re-filling that stage.  Descriptor / instruction-descriptor bit
+// layouts follow CUTLASS cute/arch/mma_sm100_desc.hpp (SmemDescriptor, InstrDescriptor).
+
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* b, u32 cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* b, u32 parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, u32 bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ u64 umma_desc(u32 saddr, u32 lbo, u32 sbo) {
+  // start>>4 [0,14) | LBO>>4 [16,30) | SBO>>4 [32,46) | version 1 [46,48) | SWIZZLE_NONE [61,64)
+  return (u64)((saddr >> 4) & 0x3FFFu) | ((u64)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((u64)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// kind::f16, A=B=bf16, D=f32, A MN-major, B K-major, N=16, M=128
+constexpr u32 UMMA_IDESC_BF16_M128_N16 =
+    (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc, u32 acc) {
+  u32 z = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(z), "r"(z), "r"(z), "r"(z));
+}
+__device__ __forceinline__ void umma_commit(u64* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(u32 taddr, u32* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// TMEM allocation by warp 0 (once per kernel); the base address lands in *slot.
+__device__ __forceinline__ u32 tmem_alloc(u32* slot, u32 ncols) {
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  return *(volatile u32*)slot;
+}
+__device__ __forceinline__ void tmem_free(u32 base, u32 ncols) {
+  tc_fence_before();
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(ncols) : "memory");
+}
+
+template <int NN, int K, int KC, int S> struct gemv_tc_layout {
+  static constexpr int NTL = (NN + 127) / 128;
+  static constexpr int NCH = NTL * 16;              // 16-byte chunks per k-row of a stage
+  static constexpr int TILE = (KC / 8) * 2048;      // bytes of one 128-column tile per stage
+  static constexpr int STAGE = NTL * TILE;
+  static constexpr int XOFF = S * STAGE;
+  static constexpr int BOFF = XOFF + 32 * K;
+  static constexpr int BYTES = BOFF + 8 * (S + 1);
+};
+
+template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, i64 SB0, i64 SB1, i64 SB2,
+          int KC, int S, int NT>
+__device__ __forceinline__ void mm_gemv_tc(float* __restrict__ out, const float* __restrict__ A,
+                                           const u16* __restrict__ B, unsigned char* __restrict__ work, u32 tmem) {
+  typedef gemv_tc_layout<NN, K, KC, S> L;
+  constexpr int NKC = K / KC;
+  static_assert(K % KC == 0 && KC % 16 == 0 && M <= 16 && NN % 8 == 0, "tcgen05 gemv shape");
+  u64* bars = reinterpret_cast<u64*>(work + L::BOFF);
+  u16* xb = reinterpret_cast<u16*>(work + L::XOFF);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int bi = 0; bi < B0 * B1; ++bi) {
+    const int b1 = bi % B1, b0 = bi / B1;
+    const float* Ab = A + b0 * SA0 + b1 * SA1;
+    const u16* Bb = B + b0 * SB0 + b1 * SB1;
+    // X^T, K-major canonical, rows M..15 zero
+    for (int e = tid; e < 16 * K; e += NT) {
+      const int kk = e & 7, m = (e >> 3) & 15, k = (e >> 7) * 8 + kk;
+      xb[e] = (m < M) ? NBF16::st(Ab[(i64)m * SA2 + (i64)k * SA3]) : (u16)0;
+    }
+    fence_async_smem();
+    if (tid == 0) {
+      for (int q = 0; q <= S; ++q) mbar_init(&bars[q], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int kc) {
+      unsigned char* st = work + (kc % S) * L::STAGE;
+      for (int c = tid; c < KC * L::NCH; c += NT) {
+        const int kk = c & 7;
+        const int rest = c >> 3;
+        const int n8 = rest % L::NCH, k8 = rest / L::NCH;
+        const int k = kc * KC + k8 * 8 + kk;
+        const bool in = n8 * 8 < NN;
+        const u16* src = Bb + (i64)k * SB2 + (in ? n8 * 8 : 0);
+        cp_async16(st + (n8 >> 4) * L::TILE + k8 * 2048 + (n8 & 15) * 128 + kk * 16, src, in ? 16u : 0u);
+      }
+      cp_async_commit();
+    };
+#pragma unroll 1
+    for (int kc = 0; kc < S - 1; ++kc) {
+      if (kc < NKC) issue(kc);
+      else cp_async_commit();
+    }
+#pragma unroll 1
+    for (int kc = 0; kc < NKC; ++kc) {
+      if (kc + S - 1 < NKC) {
+        if (kc >= 1) mbar_wait(&bars[(kc - 1) % S], ((kc - 1) / S) & 1);
+        issue(kc + S - 1);
+      } else {
+        cp_async_commit();
+      }
+      cp_async_wait<S - 1>();
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        const u32 st = smem_u32(work + (kc % S) * L::STAGE);
+        const u32 xs = smem_u32(xb);
+#pragma unroll 1
+        for (int t = 0; t < L::NTL; ++t) {
+#pragma unroll
+          for (int ks = 0; ks < KC / 16; ++ks) {
+            const u64 ad = umma_desc(st + t * L::TILE + ks * 4096, 2048, 128);
+            const u64 bd = umma_desc(xs + ((kc * KC + ks * 16) >> 3) * 256, 256, 128);
+            umma_bf16(tmem + t * 16, ad, bd, UMMA_IDESC_BF16_M128_N16, (kc | ks) != 0);
+          }
+        }
+        umma_commit(&bars[kc % S]);
+      }
+    }
+    cp_async_wait<0>();
+    mbar_wait(&bars[(NKC - 1) % S], ((NKC - 1) / S) & 1);
+    tc_fence_after();
+    // epilogue: warp w reads TMEM lanes 32*(w%4).. of tile t (D[n][m]) and writes out[m][n]
+    for (int t = warp >> 2; t < L::NTL; t += NT / 128) {
+      u32 v[16];
+      tmem_ld16(tmem + ((u32)((warp & 3) * 32) << 16) + t * 16, v);
+      const int n = t * 128 + (warp & 3) * 32 + lane;
+      if (n < NN) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) out[((i64)bi * M + m) * NN + n] = __uint_as_float(v[m]);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Cluster all-reduce as reduce-scatter + all-gather over DSMEM.  The peers of
 // a group are the ranks r with ((r ^ me) & KEEP) == 0.  Phase 1: each member
 // sums the chunk it owns from every member (DSMEM loads) into `tmp`; phase 2
