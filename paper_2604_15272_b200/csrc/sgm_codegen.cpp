@@ -760,9 +760,10 @@ struct Gen {
         if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && NN % 8 == 0 && NN >= 64 &&
             ntl <= 32 && row16 && x.sl[0] * x.sl[1] <= 8) {
           i64 kc = 16;
-          while (kc * 2 <= K && K % (kc * 2) == 0 && ntl * (kc * 2 / 8) * 2048 <= 24 * 1024) kc *= 2;
-          int S = 4;
-          i64 bytes = S * ntl * (kc / 8) * 2048 + 32 * K + 8 * (S + 1);
+          while (kc * 2 <= K && K % (kc * 2) == 0 && (kc * 2 / 8) * 2048 <= 16 * 1024) kc *= 2;
+          i64 nst = (K / kc) * ntl;
+          int S = (int)std::min<i64>(8, std::max<i64>(3, nst + 2));
+          i64 bytes = S * (kc / 8) * 2048 + 32 * K + 8 * S;
           x.tc = true;
           x.tc_kc = (int)kc;
           x.tc_s = S;

@@ -564,22 +564,27 @@ __device__ __forceinline__ void tmem_free(u32 base, u32 ncols) {
 }
 
 template <int NN, int K, int KC, int S> struct gemv_tc_layout {
-  static constexpr int NTL = (NN + 127) / 128;
-  static constexpr int NCH = NTL * 16;              // 16-byte chunks per k-row of a stage
-  static constexpr int TILE = (KC / 8) * 2048;      // bytes of one 128-column tile per stage
-  static constexpr int STAGE = NTL * TILE;
+  static constexpr int NTL = (NN + 127) / 128;     // 128-column tiles
+  static constexpr int STAGE = (KC / 8) * 2048;    // one (k-chunk, tile) stage
   static constexpr int XOFF = S * STAGE;
   static constexpr int BOFF = XOFF + 32 * K;
-  static constexpr int BYTES = BOFF + 8 * (S + 1);
+  static constexpr int BYTES = BOFF + 8 * S;
 };
 
+// Stages are (k-chunk kc, column tile t) pairs in kc-major order; D = S-2 stages
+// are in flight, and re-filling a buffer waits only on the MMAs issued two
+// stages earlier.  For M <= 8 the padded MMA rows 8..15 carry the bf16 residual
+// of A (A = hi + lo), so a computed fp32 operand keeps ~16 mantissa bits.
 template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, i64 SB0, i64 SB1, i64 SB2,
           int KC, int S, int NT>
 __device__ __forceinline__ void mm_gemv_tc(float* __restrict__ out, const float* __restrict__ A,
                                            const u16* __restrict__ B, unsigned char* __restrict__ work, u32 tmem) {
   typedef gemv_tc_layout<NN, K, KC, S> L;
-  constexpr int NKC = K / KC;
-  static_assert(K % KC == 0 && KC % 16 == 0 && M <= 16 && NN % 8 == 0, "tcgen05 gemv shape");
+  constexpr int NTL = L::NTL;
+  constexpr int NST = (K / KC) * NTL;
+  constexpr int D = S - 2;
+  constexpr bool SPLIT = M <= 8;
+  static_assert(K % KC == 0 && KC % 16 == 0 && M <= 16 && NN % 8 == 0 && S >= 3, "tcgen05 gemv shape");
   u64* bars = reinterpret_cast<u64*>(work + L::BOFF);
   u16* xb = reinterpret_cast<u16*>(work + L::XOFF);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -587,73 +592,81 @@ __device__ __forceinline__ void mm_gemv_tc(float* __restrict__ out, const float*
     const int b1 = bi % B1, b0 = bi / B1;
     const float* Ab = A + b0 * SA0 + b1 * SA1;
     const u16* Bb = B + b0 * SB0 + b1 * SB1;
-    // X^T, K-major canonical, rows M..15 zero
+    // A^T, K-major canonical: rows 0..M-1 = bf16(a); rows 8..8+M-1 = bf16(a - hi) when SPLIT
     for (int e = tid; e < 16 * K; e += NT) {
       const int kk = e & 7, m = (e >> 3) & 15, k = (e >> 7) * 8 + kk;
-      xb[e] = (m < M) ? NBF16::st(Ab[(i64)m * SA2 + (i64)k * SA3]) : (u16)0;
+      u16 v = 0;
+      if (m < M) {
+        v = NBF16::st(Ab[(i64)m * SA2 + (i64)k * SA3]);
+      } else if (SPLIT && m >= 8 && m - 8 < M) {
+        const float a = Ab[(i64)(m - 8) * SA2 + (i64)k * SA3];
+        v = NBF16::st(a - NBF16::ld(NBF16::st(a)));
+      }
+      xb[e] = v;
     }
     fence_async_smem();
     if (tid == 0) {
-      for (int q = 0; q <= S; ++q) mbar_init(&bars[q], 1);
+      for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    auto issue = [&](int kc) {
-      unsigned char* st = work + (kc % S) * L::STAGE;
-      for (int c = tid; c < KC * L::NCH; c += NT) {
+    auto issue = [&](int s) {
+      const int kc = s / NTL, t = s % NTL;
+      unsigned char* st = work + (s % S) * L::STAGE;
+      for (int c = tid; c < KC * 16; c += NT) {
         const int kk = c & 7;
-        const int rest = c >> 3;
-        const int n8 = rest % L::NCH, k8 = rest / L::NCH;
+        const int n8 = (c >> 3) & 15, k8 = c >> 7;
         const int k = kc * KC + k8 * 8 + kk;
-        const bool in = n8 * 8 < NN;
-        const u16* src = Bb + (i64)k * SB2 + (in ? n8 * 8 : 0);
-        cp_async16(st + (n8 >> 4) * L::TILE + k8 * 2048 + (n8 & 15) * 128 + kk * 16, src, in ? 16u : 0u);
+        const int col = t * 128 + n8 * 8;
+        const bool in = col < NN;
+        cp_async16(st + k8 * 2048 + n8 * 128 + kk * 16, Bb + (i64)k * SB2 + (in ? col : 0), in ? 16u : 0u);
       }
       cp_async_commit();
     };
 #pragma unroll 1
-    for (int kc = 0; kc < S - 1; ++kc) {
-      if (kc < NKC) issue(kc);
+    for (int s = 0; s < D; ++s) {
+      if (s < NST) issue(s);
       else cp_async_commit();
     }
 #pragma unroll 1
-    for (int kc = 0; kc < NKC; ++kc) {
-      if (kc + S - 1 < NKC) {
-        if (kc >= 1) mbar_wait(&bars[(kc - 1) % S], ((kc - 1) / S) & 1);
-        issue(kc + S - 1);
+    for (int s = 0; s < NST; ++s) {
+      const int nx = s + D;  // refill: its buffer last served stage nx - S (MMAs issued 2 stages ago)
+      if (nx < NST) {
+        if (nx - S >= 0) mbar_wait(&bars[nx % S], ((nx - S) / S) & 1);
+        issue(nx);
       } else {
         cp_async_commit();
       }
-      cp_async_wait<S - 1>();
+      cp_async_wait<D>();
       fence_async_smem();
       __syncthreads();
       if (tid == 0) {
         tc_fence_after();
-        const u32 st = smem_u32(work + (kc % S) * L::STAGE);
+        const int kc = s / NTL, t = s % NTL;
+        const u32 st = smem_u32(work + (s % S) * L::STAGE);
         const u32 xs = smem_u32(xb);
-#pragma unroll 1
-        for (int t = 0; t < L::NTL; ++t) {
 #pragma unroll
-          for (int ks = 0; ks < KC / 16; ++ks) {
-            const u64 ad = umma_desc(st + t * L::TILE + ks * 4096, 2048, 128);
-            const u64 bd = umma_desc(xs + ((kc * KC + ks * 16) >> 3) * 256, 256, 128);
-            umma_bf16(tmem + t * 16, ad, bd, UMMA_IDESC_BF16_M128_N16, (kc | ks) != 0);
-          }
+        for (int ks = 0; ks < KC / 16; ++ks) {
+          const u64 ad = umma_desc(st + ks * 4096, 2048, 128);
+          const u64 bd = umma_desc(xs + ((kc * KC + ks * 16) >> 3) * 256, 256, 128);
+          umma_bf16(tmem + t * 16, ad, bd, UMMA_IDESC_BF16_M128_N16, (kc | ks) != 0);
         }
-        umma_commit(&bars[kc % S]);
+        umma_commit(&bars[s % S]);
       }
     }
     cp_async_wait<0>();
-    mbar_wait(&bars[(NKC - 1) % S], ((NKC - 1) / S) & 1);
+    mbar_wait(&bars[(NST - 1) % S], ((NST - 1) / S) & 1);
     tc_fence_after();
     // epilogue: warp w reads TMEM lanes 32*(w%4).. of tile t (D[n][m]) and writes out[m][n]
-    for (int t = warp >> 2; t < L::NTL; t += NT / 128) {
+    for (int t = warp >> 2; t < NTL; t += NT / 128) {
       u32 v[16];
       tmem_ld16(tmem + ((u32)((warp & 3) * 32) << 16) + t * 16, v);
       const int n = t * 128 + (warp & 3) * 32 + lane;
       if (n < NN) {
 #pragma unroll
-        for (int m = 0; m < M; ++m) out[((i64)bi * M + m) * NN + n] = __uint_as_float(v[m]);
+        for (int m = 0; m < M; ++m)
+          out[((i64)bi * M + m) * NN + n] = SPLIT ? __uint_as_float(v[m]) + __uint_as_float(v[8 + m])
+                                                  : __uint_as_float(v[m]);
       }
     }
     tc_fence_before();
