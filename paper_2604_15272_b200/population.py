@@ -223,12 +223,16 @@ def argmin(records: list) -> Optional[Record]:
 
 
 def reduce_best(best: Optional[Record], dist) -> int:
-    """all_reduce(MIN) of (latency_ns << 20 | index) across ranks; returns the global winner index."""
+    """all_reduce(MIN) of (latency_ns << 20 | index) across ranks; returns the global winner index.
+    Ties on latency resolve to the smaller population index, like tune()'s lexicographic
+    (score, params) tie-break (tuner.py:221-223).  NCCL over NVLink on the GPU box; the
+    same call runs on gloo (CPU tensors) in the multi-process tests."""
     t = torch()
     key = (1 << 62) if best is None else (int(round(best.latency_us * 1000)) << 20) | best.index
     if dist is None:
         return -1 if best is None else best.index
-    x = t.tensor([key], dtype=t.int64, device=f"cuda:{t.cuda.current_device()}")
+    dev = f"cuda:{t.cuda.current_device()}" if dist.get_backend() == "nccl" else "cpu"
+    x = t.tensor([key], dtype=t.int64, device=dev)
     dist.all_reduce(x, op=dist.ReduceOp.MIN)
     v = int(x.item())
     return -1 if v >= (1 << 62) else (v & ((1 << 20) - 1))
