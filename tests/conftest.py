@@ -42,3 +42,20 @@ def case_inputs_ff(case):
     names = [t for t in prog["tensors"] if t["role"] == "input"]
     return {t["name"]: ff_np.ff_uniform(int(np.prod(t["dims"])), ff_trial_seed(0, case["cid"], 0), k + 1)
             .reshape(tuple(t["dims"])) for k, t in enumerate(names)}
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_symfuse():
+    """The unmodified reference package installed into baseline/_ref (travels to the
+    GPU box with the snapshot); None when it was not installed."""
+    if not os.path.isdir(os.path.join(REF_DIR, "symfuse")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.append(REF_DIR)
+    try:
+        import symfuse
+        return symfuse
+    except ImportError:
+        return None
