@@ -11,8 +11,10 @@ Candidates are sharded over ranks (LPT), so `scaling` is "strong".
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
 
---impl reference times the reference's CPU path (the oracle port of
-symfuse interp.run_concrete / run_program, numpy fp64) on the host cores.
+--impl reference times the reference's CPU path on the host cores: the
+unmodified symfuse interp.run_concrete / run_program (numpy fp64) installed in
+baseline/_ref, with the oracle port of the same functions for the one workload
+the reference cannot express (G at 14336).
 """
 from __future__ import annotations
 
@@ -92,17 +94,78 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- CPU arm
 
 
+def _reference_symfuse():
+    """The unmodified reference (symfuse) installed into baseline/_ref, if present."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "symfuse")):
+        return None
+    if ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        import symfuse.interp  # noqa: F401
+        return sys.modules["symfuse"]
+    except Exception:
+        return None
+
+
+class _RefPath:
+    """One candidate evaluation on the reference's own CPU path: score_interp-style
+    timed symfuse.interp.run_concrete + one random_equiv_test trial (run_program +
+    run_concrete + rel_err, interp.py:272-283).  Workloads the reference cannot
+    express (G at 14336: TensorSpec rejects non-powers of two, graph.py:96-101)
+    run on the oracle port of the same functions instead."""
+
+    def __init__(self, pops):
+        self.sf = _reference_symfuse()
+        self.progs = {}
+        self.kinds = set()
+        if self.sf is not None:
+            from symfuse.graph import ProgOp, Program, TensorSpec
+            from fractions import Fraction
+            for w, pop in pops.items():
+                pd = pop["program"]
+                try:
+                    self.progs[w] = Program(
+                        pd["name"], tuple(TensorSpec(t["name"], tuple(t["dims"]), t["role"]) for t in pd["tensors"]),
+                        tuple(ProgOp(o["kind"], tuple(o["inputs"]), o["out"], o.get("axis"),
+                                     Fraction(*o["const"]) if "const" in o else None) for o in pd["ops"]),
+                        tuple(pd["outputs"]))
+                except Exception:
+                    pass
+
+    def evaluate(self, u, prog_dict, ins):
+        from oracle import block_np
+        from paper_2604_15272_b200 import ir
+        key = ir.template_key(u.cand)
+        if u.workload in self.progs:
+            from symfuse.graph import deserialize, instantiate
+            from symfuse.interp import rel_err, run_concrete, run_program
+            program = self.progs[u.workload]
+            g, m, _ = deserialize(key, program)
+            conc = instantiate(g, m, u.cand.params)
+            run_concrete(conc, ins)                      # score_interp run (tuner.py:171-173)
+            got = run_concrete(conc, ins)                # equivalence trial (interp.py:277-283)
+            exp = run_program(program, ins)
+            max(rel_err(got[n], exp[n]) for n in program.outputs)
+            self.kinds.add("reference")
+            return
+        block_np.run_concrete(prog_dict, key, u.cand.params, ins)
+        got = block_np.run_concrete(prog_dict, key, u.cand.params, ins)
+        exp = block_np.run_program(prog_dict, ins)
+        max(block_np.rel_err(got[n], exp[n]) for n in prog_dict["outputs"])
+        self.kinds.add("port")
+
+
 def cpu_eval_sample(seconds: float, workloads, seed: int = 0) -> dict:
-    """The reference's CPU candidate evaluation (oracle port of interp.run_concrete /
-    run_program, numpy fp64) on a bounded sample of the population:
+    """The reference's CPU candidate evaluation (symfuse interp.run_concrete /
+    run_program in fp64 numpy) on a bounded sample of the population:
     per candidate one timed run_concrete (score_interp) + one equivalence trial."""
     import numpy as np
 
-    from oracle import block_np
-    from paper_2604_15272_b200 import ir
     from paper_2604_15272_b200 import population as P
 
     pops = {w: P.load_population(w) for w in workloads}
+    path = _RefPath(pops)
     order = []
     per = {w: P.units(pops[w]) for w in workloads}
     k = 0
@@ -118,21 +181,22 @@ def cpu_eval_sample(seconds: float, workloads, seed: int = 0) -> dict:
     for u in order:
         if time.perf_counter() - t0 > seconds and done:
             break
-        pop = pops[u.workload]
-        prog = pop["program"]
+        prog = pops[u.workload]["program"]
         if u.workload not in inputs:
             inputs[u.workload] = {t["name"]: rng.standard_normal(tuple(t["dims"])) for t in prog["tensors"]
                                   if t["role"] == "input"}
-        ins = inputs[u.workload]
-        key = ir.template_key(u.cand)
-        block_np.run_concrete(prog, key, u.cand.params, ins)          # score_interp run
-        got = block_np.run_concrete(prog, key, u.cand.params, ins)    # equivalence trial
-        exp = block_np.run_program(prog, ins)
-        max(block_np.rel_err(got[n], exp[n]) for n in prog["outputs"])
+        path.evaluate(u, prog, inputs[u.workload])
         done += 1
     el = time.perf_counter() - t0
-    return {"candidates": done, "seconds": el, "value": done / el,
-            "sample": f"{done} candidates round-robin over {','.join(workloads)} (fp64 numpy, full scale)"}
+    kind = "reference" if path.kinds == {"reference"} else ("port" if path.kinds == {"port"} else "reference+port")
+    try:
+        import threadpoolctl
+        blas = [f"{d.get('internal_api')}:{d.get('num_threads')}thr" for d in threadpoolctl.threadpool_info()]
+    except Exception:
+        blas = []
+    return {"candidates": done, "seconds": el, "value": done / el, "kind": kind,
+            "sample": f"{done} candidates round-robin over {','.join(workloads)} (fp64 numpy, full scale; "
+                      f"symfuse from baseline/_ref where expressible, oracle port otherwise; BLAS {blas})"}
 
 
 def reference_arm(args) -> None:
@@ -149,13 +213,14 @@ def reference_arm(args) -> None:
         cands += r["candidates"]
         secs += r["seconds"]
         sample = r["sample"]
+        kind = r["kind"]
     v = cands / secs
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1000,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": "five-workload SIGMA population (R,G,A,Q,L)",
-                                            "path": "oracle port of symfuse interp (CPU)"},
-            "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": os.cpu_count(), "kind": "port",
+                                            "path": "symfuse interp (CPU, baseline/_ref) + oracle port for G@14336"},
+            "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": os.cpu_count(), "kind": kind,
                              "sample": sample},
             "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -368,7 +433,7 @@ def main() -> None:
         l0 = _abi.launch_count()
         r = cpu_eval_sample(20.0, args.workloads)
         assert _abi.launch_count() == l0
-        cpu = {"value": r["value"], "unit": "candidates/s", "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": r["value"], "unit": "candidates/s", "cores": os.cpu_count(), "kind": r["kind"],
                "sample": r["sample"]}
     line = {
         "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world, "steps": args.steps,

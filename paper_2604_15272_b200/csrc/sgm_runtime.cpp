@@ -166,6 +166,12 @@ struct DevState {
   CUmodule util = nullptr;
   CUfunction f_fill64, f_fill32, f_fill16, f_ff_fill, f_cmp, f_re64, f_re32, f_re16, f_n64, f_n32, f_n16;
   CUdeviceptr red = 0;  // 4 x u64 reduction scratch
+  // host-buffer (e2e) staging shared by every plan of this device: pinned host
+  // memory + one device buffer, grown on demand (sgm_plan_run_host)
+  std::mutex io_mu;
+  void* pinned = nullptr;
+  CUdeviceptr dev_io = 0;
+  size_t io_bytes = 0;
 };
 DevState g_dev[16];
 thread_local int t_device = -1;
@@ -300,11 +306,6 @@ struct sgm_plan {
   int64_t out_elems[SGM_MAX_SLOTS] = {0};
   double compile_ms = 0;
   int cache_hit = 0;
-  // e2e staging
-  void* pinned = nullptr;
-  size_t pinned_bytes = 0;
-  CUdeviceptr dev_io = 0;
-  size_t dev_io_bytes = 0;
   CUstream tstream = nullptr;
 };
 
@@ -448,12 +449,10 @@ int sgm_plan_source(const sgm_plan* p, char* buf, size_t cap, size_t* len) {
 
 int sgm_plan_destroy(sgm_plan* p) {
   if (!p) return SGM_OK;
-  if (p->mod || p->scratch || p->pinned || p->dev_io || p->tstream) {
+  if (p->mod || p->scratch || p->tstream) {
     if (D.ok && p->device >= 0 && g_dev[p->device].init) D.cuCtxSetCurrent(g_dev[p->device].ctx);
     if (p->mod) D.cuModuleUnload(p->mod);
     if (p->scratch) D.cuMemFree(p->scratch);
-    if (p->dev_io) D.cuMemFree(p->dev_io);
-    if (p->pinned) D.cuMemFreeHost(p->pinned);
     if (p->tstream) D.cuStreamDestroy(p->tstream);
   }
   delete p;
@@ -508,41 +507,44 @@ int sgm_plan_run_host(sgm_plan* p, const void* const* host_inputs, void* const* 
   size_t tot = 0;
   for (int k = 0; k < p->n_in; ++k) tot += (p->in_bytes[k] + 255) / 256 * 256;
   for (int k = 0; k < p->n_out; ++k) tot += (p->out_bytes[k] + 255) / 256 * 256;
-  if (tot > p->pinned_bytes) {
-    if (p->pinned) D.cuMemFreeHost(p->pinned);
-    if (p->dev_io) D.cuMemFree(p->dev_io);
-    p->pinned = nullptr;
-    p->dev_io = 0;
-    CU(D.cuMemHostAlloc(&p->pinned, tot, 0));
-    CU(D.cuMemAlloc(&p->dev_io, tot));
-    p->pinned_bytes = p->dev_io_bytes = tot;
+  DevState& S = g_dev[p->device];
+  std::lock_guard<std::mutex> lk(S.io_mu);
+  if (tot > S.io_bytes) {
+    if (S.pinned) D.cuMemFreeHost(S.pinned);
+    if (S.dev_io) D.cuMemFree(S.dev_io);
+    S.pinned = nullptr;
+    S.dev_io = 0;
+    S.io_bytes = 0;
+    CU(D.cuMemHostAlloc(&S.pinned, tot, 0));
+    CU(D.cuMemAlloc(&S.dev_io, tot));
+    S.io_bytes = tot;
   }
   CUstream s = (CUstream)stream;
   const void* din[SGM_MAX_SLOTS];
   void* dout[SGM_MAX_SLOTS];
   size_t off = 0;
   for (int k = 0; k < p->n_in; ++k) {
-    memcpy((char*)p->pinned + off, host_inputs[k], p->in_bytes[k]);
-    CU(D.cuMemcpyHtoDAsync(p->dev_io + off, (char*)p->pinned + off, p->in_bytes[k], s));
-    din[k] = (const void*)(p->dev_io + off);
+    memcpy((char*)S.pinned + off, host_inputs[k], p->in_bytes[k]);
+    CU(D.cuMemcpyHtoDAsync(S.dev_io + off, (char*)S.pinned + off, p->in_bytes[k], s));
+    din[k] = (const void*)(S.dev_io + off);
     off += (p->in_bytes[k] + 255) / 256 * 256;
   }
   size_t out0 = off;
   for (int k = 0; k < p->n_out; ++k) {
-    dout[k] = (void*)(p->dev_io + off);
+    dout[k] = (void*)(S.dev_io + off);
     if ((st = fill_nan(p->numsys, (CUdeviceptr)dout[k], p->out_elems[k], s))) return st;
     off += (p->out_bytes[k] + 255) / 256 * 256;
   }
   if ((st = launch_plan(p, din, dout, s))) return st;
   off = out0;
   for (int k = 0; k < p->n_out; ++k) {
-    CU(D.cuMemcpyDtoHAsync((char*)p->pinned + off, (CUdeviceptr)dout[k], p->out_bytes[k], s));
+    CU(D.cuMemcpyDtoHAsync((char*)S.pinned + off, (CUdeviceptr)dout[k], p->out_bytes[k], s));
     off += (p->out_bytes[k] + 255) / 256 * 256;
   }
   CU(D.cuStreamSynchronize(s));
   off = out0;
   for (int k = 0; k < p->n_out; ++k) {
-    memcpy(host_outputs[k], (char*)p->pinned + off, p->out_bytes[k]);
+    memcpy(host_outputs[k], (char*)S.pinned + off, p->out_bytes[k]);
     off += (p->out_bytes[k] + 255) / 256 * 256;
   }
   return SGM_OK;
