@@ -119,7 +119,8 @@ typedef struct {
   int32_t no_loop_split;   /* 1: run the for-loop sequentially inside every CTA */
   int32_t no_hoist;        /* 1: do not hoist loop-invariant body nodes */
   int32_t use_tcgen05;     /* -1 off, 0 auto, 1 force where legal */
-  int32_t _reserved[9];
+  int32_t no_tma;          /* 1: stream matmul operands with plain loads, no TMA producer warp */
+  int32_t _reserved[8];
 } sgm_plan_hints;
 
 typedef struct {

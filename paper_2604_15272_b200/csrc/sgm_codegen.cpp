@@ -93,6 +93,9 @@ struct Node {
   int at_off = 0;
   bool tc = false;   // tcgen05 realisation (bf16)
   int tc_kc = 16, tc_s = 4, tc_cols = 32;
+  bool tma = false;  // B streamed by the TMA producer warp through the smem ring
+  int tma_id = -1;
+  int kc = 64;       // rows of B per ring stage
 };
 
 struct Class {
@@ -151,6 +154,13 @@ struct Gen {
   int smem_peak = 0;
   i64 scratch_per_cta = 0;
   int budget = 200 * 1024;
+  // TMA producer warp + ring (any tma matmul)
+  bool prod = false;
+  bool no_tma_forced = false;
+  int ringS = 0;
+  int ring_off = 0;
+  static constexpr int kSlot = 16384;
+  static constexpr int kSmemCap = 225 * 1024;  // dynamic smem incl. ring alignment slack
 
   Gen(const sgm_plan_desc& desc, int sms) : d(desc), num_sms(sms) {}
 
@@ -705,6 +715,7 @@ struct Gen {
 
   // matmul realisation choices (depend on slices)
   void matmul_choices() {
+    int ntma = 0;
     for (int n = 0; n < (int)nodes.size(); ++n) {
       Node& x = nodes[n];
       if (x.kind != SGM_MATMUL) continue;
@@ -773,8 +784,41 @@ struct Gen {
           x.red_bytes = 0;
           x.at_bytes = bytes;  // the tcgen05 work area re-uses the transient slot
         }
+        // TMA-fed streaming (producer warp + ring): bf16 on tcgen05, fp32 on CUDA cores
+        x.tma = false;
+        const i64 d3 = in_dims[b.slot][3];
+        const bool batch_ok = x.sl[0] * x.sl[1] <= 8 && b.sl[3] == NN && b.sl[2] == K;
+        if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 && (ns == SGM_BF16 || ns == SGM_F32)) {
+          if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && (d3 * 2) % 16 == 0 &&
+              ntl * 16 <= 512) {
+            x.tma = true;
+            ++ntma;
+            x.tc = true;
+            x.kc = K % 64 == 0 ? 64 : (K % 32 == 0 ? 32 : 16);
+            x.at_bytes = 32 * K;
+            x.red_bytes = 0;
+            int cols = 32;
+            while (cols < ntl * 16) cols *= 2;
+            x.tc_cols = cols;
+          } else if (ns == SGM_F32 && M <= 8 && K % 8 == 0 && (d3 * 4) % 16 == 0) {
+            x.tma = true;
+            ++ntma;
+            x.tc = false;
+            x.kc = K % 64 == 0 ? 64 : (K % 32 == 0 ? 32 : (K % 16 == 0 ? 16 : 8));
+            i64 a0 = (a.sl[0] > 1) ? x.sl[0] : 1, a1 = (a.sl[1] > 1) ? x.sl[1] : 1;
+            x.at_bytes = a0 * a1 * K * M * 4;
+            x.red_bytes = (i64)(NT / 32) * M * 64 * 4;
+          }
+        }
       }
     }
+    prod = false;
+    int id = 0;
+    for (auto& x : nodes)
+      if (x.kind == SGM_MATMUL && x.tma) {
+        prod = true;
+        x.tma_id = id++;
+      }
   }
 
   // liveness-based smem allocation; returns peak bytes
@@ -887,7 +931,8 @@ struct Gen {
       schedule();
       matmul_choices();
       smem_peak = allocate();
-      if (smem_peak <= budget) return true;
+      const int tile_budget = prod ? std::min(budget, kSmemCap - (3 * kSlot + 1024)) : budget;
+      if (smem_peak <= tile_budget) return true;
       // largest smem tile
       int big = -1;
       i64 bb = 0;
@@ -928,7 +973,23 @@ struct Gen {
       if (sp < 0) break;
       nodes[sp].store = ST_GLOBAL;
     }
-    return smem_peak <= budget;
+    return smem_peak <= (prod ? std::min(budget, kSmemCap - (3 * kSlot + 1024)) : budget);
+  }
+
+  // ring geometry after the tile plan: as many 16 KB slots as fit (<= 12), capped so
+  // that two CTAs share an SM when the grid exceeds one wave
+  void plan_ring() {
+    if (!prod) { ringS = 0; return; }
+    int base = (smem_peak + 1023) / 1024 * 1024;
+    int S = std::min(12, (kSmemCap - base - 1024) / kSlot);
+    i64 ctas = LB * FP * CL;
+    if (ctas > num_sms) {
+      int S2 = (113 * 1024 - base - 1024) / kSlot;
+      if (S2 >= 4) S = std::min(S, S2);
+    }
+    ringS = S;
+    ring_off = base;
+    smem_peak = base + 1024 + S * kSlot;
   }
 
   // ------------------------------------------------------------ emission
@@ -980,6 +1041,85 @@ struct Gen {
     return e.str();
   }
 
+  // start index along padded dim k of a loader tile slice (same nesting as offset_expr)
+  std::string coord_expr(const Node& x, int k, const std::string& jexpr) const {
+    const i64* dims = in_dims[x.slot];
+    static const char* gv[3] = {"gx", "gy", "gz"};
+    i64 w = dims[k];
+    std::ostringstream e;
+    e << "0";
+    if (w <= 1) return e.str();
+    for (int g = 0; g < ngrid; ++g)
+      if (x.gmask[k] >> g & 1u) {
+        w /= grid[g];
+        e << " + (int)" << gv[g] << " * " << w;
+      }
+    if (x.lsplit[k]) {
+      w /= nloop;
+      e << " + (int)(" << jexpr << ") * " << w;
+    }
+    int c = x.cls[k];
+    if (c >= 0 && cls[c].parts > 1) e << " + " << part_var(c) << " * " << (x.sh[k] / cls[c].parts);
+    return e.str();
+  }
+
+  // producer-side stage sequence of one streamed matmul (mirrors mm_stream_tc / mm_stream_f32)
+  void emit_producer_node(int n, bool in_loop) {
+    const Node& x = nodes[n];
+    const Node& a = nodes[x.in[0]];
+    const Node& b = nodes[x.in[1]];
+    std::string J = in_loop ? "j" : std::to_string(nloop - 1);
+    i64 K = a.sl[3], NN = x.sl[3];
+    os << "      { // stream for node " << n << "\n";
+    os << "        const int c0 = " << coord_expr(b, 3, J) << ", c1 = " << coord_expr(b, 2, J) << ", c2 = "
+       << coord_expr(b, 1, J) << ", c3 = " << coord_expr(b, 0, J) << ";\n";
+    os << "        for (int bi = 0; bi < " << x.sl[0] * x.sl[1] << "; ++bi) {\n";
+    os << "          const int d2 = c2 + " << (b.sl[1] > 1 ? "bi % " + std::to_string(x.sl[1]) : std::string("0"))
+       << ", d3 = c3 + " << (b.sl[0] > 1 ? "bi / " + std::to_string(x.sl[1]) : std::string("0")) << ";\n";
+    if (x.tc) {
+      i64 ntl = (NN + 127) / 128;
+      os << "          for (int kc = 0; kc < " << K / x.kc << "; ++kc)\n";
+      os << "            for (int t = 0; t < " << ntl << "; ++t) {\n";
+      os << "              const unsigned slot = sgm::ring_acquire<" << ringS << ">(empty, pq++);\n";
+      os << "              const int nb = (" << NN << " - t * 128 > 64) ? 2 : 1;\n";
+      os << "              sgm::mbar_expect_tx(&full[slot], nb * " << x.kc * 128 << ");\n";
+      os << "              unsigned char* dst = ring + slot * sgm::SLOT;\n";
+      os << "              sgm::tma_load_4d(dst, &a.tm[" << x.tma_id << "], c0 + t * 128, c1 + kc * " << x.kc
+         << ", d2, d3, &full[slot]);\n";
+      os << "              if (nb == 2) sgm::tma_load_4d(dst + " << x.kc * 128 << ", &a.tm[" << x.tma_id
+         << "], c0 + t * 128 + 64, c1 + kc * " << x.kc << ", d2, d3, &full[slot]);\n";
+      os << "            }\n";
+    } else {
+      i64 nt64 = (NN + 63) / 64;
+      os << "          for (int t = 0; t < " << nt64 << "; ++t)\n";
+      os << "            for (int kc = 0; kc < " << K / x.kc << "; ++kc) {\n";
+      os << "              const unsigned slot = sgm::ring_acquire<" << ringS << ">(empty, pq++);\n";
+      os << "              sgm::mbar_expect_tx(&full[slot], " << x.kc * 256 << ");\n";
+      os << "              sgm::tma_load_4d(ring + slot * sgm::SLOT, &a.tm[" << x.tma_id << "], c0 + t * 64, c1 + kc * "
+         << x.kc << ", d2, d3, &full[slot]);\n";
+      os << "            }\n";
+    }
+    os << "        }\n      }\n";
+  }
+
+  void emit_producer() {
+    os << "    if (tid == NT) {\n      unsigned pq = 0;\n";
+    bool in_loop = false;
+    for (int p = 0; p < (int)sched.size(); ++p) {
+      const Ev& e = sched[p];
+      if (e.type == Ev::LOOP_BEGIN) {
+        os << "      for (int j = jp; j < " << nloop << "; j += " << LP << ") {\n";
+        in_loop = true;
+      } else if (e.type == Ev::LOOP_END) {
+        os << "      }\n";
+        in_loop = false;
+      } else if (e.type == Ev::NODE && nodes[e.node].kind == SGM_MATMUL && nodes[e.node].tma) {
+        emit_producer_node(e.node, in_loop);
+      }
+    }
+    os << "    }\n    return;\n";
+  }
+
   // vector width for a loader (x) or a saver (x = saver node, sl = its input's slice)
   int io_vec(const Node& x, bool loader, const i64* sl = nullptr) const {
     const i64* dims = loader ? in_dims[x.slot] : out_dims[x.slot];
@@ -1028,23 +1168,28 @@ struct Gen {
     return p.str();
   }
 
+  std::string cl_sync() const {
+    if (prod) return "    sgm::cl_barrier<NT, " + std::to_string(CL) + ">(clbar, sclph);\n";
+    return "    sgm::cluster_sync();\n";
+  }
+
   void emit_flush(const std::vector<int>& fl, int pos) {
     // reduce-scatter (DSMEM loads into tmp) + all-gather (DSMEM stores)
-    os << "    sgm::cluster_sync();\n";
+    os << cl_sync();
     for (int f : fl) {
       const Node& x = nodes[f];
       u32 keep = (u32)(CL - 1) & ~x.pend;
       os << "    sgm::cl_rs_phase1<N, " << prod4(x.sl) << ", " << CL << ", " << keep << "u, NT>(" << tile_ptr(f)
          << ", (C*)(sm + " << flush_tmp_off.at({pos, f}) << "), crank);\n";
     }
-    os << "    sgm::cluster_sync();\n";
+    os << cl_sync();
     for (int f : fl) {
       const Node& x = nodes[f];
       u32 keep = (u32)(CL - 1) & ~x.pend;
       os << "    sgm::cl_rs_phase2<N, " << prod4(x.sl) << ", " << CL << ", " << keep << "u, NT>(" << tile_ptr(f)
          << ", (const C*)(sm + " << flush_tmp_off.at({pos, f}) << "), crank);\n";
     }
-    os << "    sgm::cluster_sync();\n";
+    os << cl_sync();
   }
 
   void emit_node(int n, bool in_loop) {
@@ -1134,7 +1279,17 @@ struct Gen {
         };
         std::string pa = a.store == ST_VIEW ? view_ptr(a) : tile_ptr(x.in[0]);
         std::string pb = b.store == ST_VIEW ? view_ptr(b) : tile_ptr(x.in[1]);
-        if (x.gemv && x.tc) {
+        if (x.tma && x.tc) {
+          os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
+             << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS
+             << ", NT>(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
+             << ", tmem_base, ring, full, empty, done, sq, sdph);\n";
+        } else if (x.tma) {
+          os << "    sgm::mm_stream_f32<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
+             << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS
+             << ", NT>(" << tile_ptr(n) << ", " << pa << ", (float*)(sm + " << x.at_off << "), (float*)(sm + "
+             << x.red_off << "), ring, full, empty, sq);\n";
+        } else if (x.gemv && x.tc) {
           os << "    sgm::mm_gemv_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << sb[0] << "LL, " << sb[1]
              << "LL, " << sb[2] << "LL, " << x.tc_kc << ", " << x.tc_s << ", NT>(" << tile_ptr(n) << ", " << pa
@@ -1157,7 +1312,7 @@ struct Gen {
       }
       default: break;
     }
-    os << "    __syncthreads();\n";
+    os << "    sgm::csync<NT>();\n";
   }
 
   void emit() {
@@ -1166,10 +1321,10 @@ struct Gen {
        << ", loop parts " << LP << "\n";
     os << "typedef " << nstruct() << " N;\ntypedef N::S S;\ntypedef N::C C;\ntypedef N::A A;\n";
     os << "#define NT " << NT << "\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(NT)";
+    os << "extern \"C\" __global__ void __launch_bounds__(" << (prod ? NT + 32 : NT) << ")";
     if (CL > 1) os << " __cluster_dims__(" << CL << ", 1, 1)";
-    os << " @KNAME@(const sgm::Args a) {\n";
-    os << "  extern __shared__ __align__(128) unsigned char sm[];\n";
+    os << " @KNAME@(const __grid_constant__ sgm::Args a) {\n";
+    os << "  extern __shared__ __align__(1024) unsigned char sm[];\n";
     os << "  const int tid = threadIdx.x;\n";
     os << "  const long long bid = blockIdx.x;\n";
     if (CL > 1) os << "  const unsigned crank = sgm::cluster_rank();\n";
@@ -1200,12 +1355,38 @@ struct Gen {
       else if (x.store == ST_GLOBAL)
         os << "  C* " << tile_ptr(n) << " = (C*)(scr + " << x.off << ");\n";
     }
+    if (prod) {
+      // ring barriers; the producer warp (threads NT..NT+31) runs ahead of the compute warps
+      os << "  __shared__ __align__(8) unsigned long long sgm_bars[" << 2 * ringS + 2 << "];\n";
+      os << "  unsigned long long* full = sgm_bars;\n  unsigned long long* empty = sgm_bars + " << ringS
+         << ";\n  unsigned long long* done = sgm_bars + " << 2 * ringS << ";\n  unsigned long long* clbar = sgm_bars + "
+         << 2 * ringS + 1 << ";\n  (void)done; (void)clbar;\n";
+      os << "  unsigned char* ring = sm + " << ring_off << ";\n";
+      os << "  ring += (1024u - (sgm::smem_u32(ring) & 1023u)) & 1023u;\n";
+      bool any_tc = false;
+      for (auto& x : nodes) any_tc = any_tc || (x.kind == SGM_MATMUL && x.tma && x.tc);
+      os << "  if (tid == 0) {\n";
+      os << "    for (int q = 0; q < " << ringS << "; ++q) { sgm::mbar_init(&full[q], 1); sgm::mbar_init(&empty[q], "
+         << (any_tc ? 1 : NT / 32) << "); }\n";
+      os << "    sgm::mbar_init(done, 1);\n    sgm::mbar_init(clbar, " << CL << ");\n";
+      os << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
+      os << "  if (tid == NT) {\n";
+      for (auto& x : nodes)
+        if (x.kind == SGM_MATMUL && x.tma) os << "    sgm::tma_prefetch_desc(&a.tm[" << x.tma_id << "]);\n";
+      os << "  }\n";
+      os << "  __syncthreads();\n";
+      if (CL > 1) os << "  sgm::cluster_sync();\n";
+      os << "  if (tid >= NT) {\n";
+      emit_producer();
+      os << "  }\n";
+      os << "  unsigned sq = 0, sdph = 0, sclph = 0; (void)sq; (void)sdph; (void)sclph;\n";
+    }
     int tmem_cols = 0;
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) tmem_cols = std::max(tmem_cols, x.tc_cols);
     if (tmem_cols) {
       os << "  __shared__ unsigned tmem_slot;\n";
-      os << "  const unsigned tmem_base = sgm::tmem_alloc(&tmem_slot, " << tmem_cols << "u);\n";
+      os << "  const unsigned tmem_base = sgm::tmem_alloc<NT>(&tmem_slot, " << tmem_cols << "u);\n";
     }
     bool in_loop = false;
     for (int p = 0; p < (int)sched.size(); ++p) {
@@ -1214,7 +1395,7 @@ struct Gen {
         for (int n = 0; n < (int)nodes.size(); ++n)
           if (nodes[n].kind == SGM_ACCUM)
             os << "  for (int e = tid; e < " << prod4(nodes[n].sl) << "; e += NT) " << tile_ptr(n) << "[e] = N::zero();\n";
-        os << "  __syncthreads();\n";
+        os << "  sgm::csync<NT>();\n";
         os << "  for (int j = jp; j < " << nloop << "; j += " << LP << ") {\n";
         in_loop = true;
       } else if (e.type == Ev::LOOP_END) {
@@ -1226,7 +1407,7 @@ struct Gen {
         emit_node(e.node, in_loop);
       }
     }
-    if (tmem_cols) os << "  sgm::tmem_free(tmem_base, " << tmem_cols << "u);\n";
+    if (tmem_cols) os << "  sgm::tmem_free<NT>(tmem_base, " << tmem_cols << "u);\n";
     os << "}\n";
   }
 
@@ -1235,7 +1416,13 @@ struct Gen {
     structure();
     decide_views();
     split_plan();
-    if (!fit()) {
+    bool ok = fit();
+    if (!ok && prod) {  // the ring does not fit next to the tiles: plain streamed loads
+      no_tma_forced = true;
+      ok = fit();
+    }
+    plan_ring();
+    if (!ok) {
       // still over budget after spilling everything spillable; the hard cap leaves
       // room for the templates' static smem under the 227 KB opt-in limit
       if (smem_peak > 224 * 1024) {
@@ -1256,20 +1443,34 @@ struct Gen {
     R.cluster = CL;
     R.free_parts = FP;
     R.ctas = LB * FP * CL;
-    R.threads = NT;
+    R.threads = prod ? NT + 32 : NT;
+    R.ring_slots = ringS;
+    for (auto& x : nodes) {
+      if (x.kind != SGM_MATMUL || !x.tma) continue;
+      R.n_tma++;
+      const Node& b = nodes[x.in[1]];
+      TmaSpec t;
+      t.slot = b.slot;
+      t.elem_bytes = es;
+      t.box0 = 64;
+      t.box1 = x.kc;
+      t.swizzle128 = x.tc ? 1 : 0;
+      for (int k = 0; k < 4; ++k) t.dims[k] = in_dims[b.slot][k];
+      R.tmaps.push_back(t);
+    }
     R.smem_bytes = smem_peak;
     R.loop_parts = LP;
     R.scratch_bytes = scratch_per_cta * R.ctas;
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) R.n_tcgen05++;
     std::ostringstream s;
-    s << "LB=" << LB << " FP=" << FP << " CL=" << CL << " LP=" << LP << " smem=" << smem_peak
+    s << "LB=" << LB << " FP=" << FP << " CL=" << CL << " LP=" << LP << " ring=" << ringS << " smem=" << smem_peak
       << " scratch/cta=" << scratch_per_cta << " classes:";
     for (int c = 0; c < (int)cls.size(); ++c)
       s << " c" << c << "(" << cls[c].extent << (cls[c].reduced ? "r" : "f") << "/" << cls[c].parts << ")";
     s << " mm:";
     for (int n = 0; n < (int)nodes.size(); ++n)
-      if (nodes[n].kind == SGM_MATMUL) s << " n" << n << (nodes[n].gemv ? (nodes[n].tc ? "tc" : "gemv") : "gen") << (nodes[n].gemv ? "/vn" + std::to_string(nodes[n].vn) + "ks" + std::to_string(nodes[n].ks) : "");
+      if (nodes[n].kind == SGM_MATMUL) s << " n" << n << (nodes[n].tma ? (nodes[n].tc ? "tma-tc" : "tma-f32") : nodes[n].gemv ? (nodes[n].tc ? "tc" : "gemv") : "gen") << (nodes[n].gemv ? "/vn" + std::to_string(nodes[n].vn) + "ks" + std::to_string(nodes[n].ks) : "");
     R.summary = s.str();
     return R;
   }

@@ -8,6 +8,17 @@
 
 namespace sgmcg {
 
+// One TMA tensor map the launch must encode: the whole input tensor `slot`
+// (rank-4, row-major, dims d[0..3] outermost first), box {box0 (innermost),
+// box1, 1, 1}.
+struct TmaSpec {
+  int slot = 0;
+  int elem_bytes = 2;   // 2: bf16, 4: fp32
+  int box0 = 64, box1 = 64;
+  int swizzle128 = 0;
+  int64_t dims[4] = {1, 1, 1, 1};
+};
+
 struct GenResult {
   int status = SGM_OK;
   std::string error;
@@ -22,6 +33,9 @@ struct GenResult {
   int64_t free_parts = 1;
   int64_t scratch_bytes = 0;   // total global scratch (all CTAs)
   int n_tcgen05 = 0;
+  int n_tma = 0;               // streamed matmuls fed by the TMA producer warp
+  int ring_slots = 0;
+  std::vector<TmaSpec> tmaps;
   std::string summary;
 };
 

@@ -22,11 +22,23 @@ typedef unsigned short u16;
 
 namespace sgm {
 
+// Opaque 128-byte TMA descriptor (CUtensorMap), encoded on the host per launch.
+struct __align__(64) TmaDesc {
+  u64 w[16];
+};
+
 struct Args {
   const void* in[16];
   void* out[16];
   void* scratch;
+  TmaDesc tm[4];
 };
+
+// Barrier among the NT compute threads only (named barrier 1).  Kernels with a
+// TMA producer warp launch NT + 32 threads; the producer never joins this.
+template <int NT> __device__ __forceinline__ void csync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // Finite field GF(p), p = 2^31 - 1 (Mersenne): 2^31 == 1 (mod p).
@@ -299,7 +311,7 @@ __device__ __forceinline__ void sum_axis(typename N::C* __restrict__ dst, const 
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) N::amerge(acc, shfl_xor(acc, off, 0xffffffffu));
     if (lane == 0) part[w] = acc;
-    __syncthreads();
+    csync<NT>();
     if (tid < OUT) {
       Acc t = N::azero();
       for (int q = 0; q < WPO; ++q) N::amerge(t, part[tid * WPO + q]);
@@ -376,7 +388,7 @@ __device__ __forceinline__ void mm_gemv(typename N::C* __restrict__ out, const t
     const int a1 = ab % A1, a0 = ab / A1;
     at[e] = A[a0 * SA0 + a1 * SA1 + (i64)m * SA2 + (i64)k * SA3];
   }
-  __syncthreads();
+  csync<NT>();
   for (int w = tid; w < WORK; w += NT) {
     const int nv = w % NV;
     const int ks = (w / NV) % KS;
@@ -468,7 +480,7 @@ __device__ __forceinline__ void mm_gemv(typename N::C* __restrict__ out, const t
     }
   }
   if constexpr (LY::KS_OUT > 1) {
-    __syncthreads();
+    csync<NT>();
     for (int e = tid; e < ITEMS * M * VN; e += NT) {
       Acc t = N::azero();
 #pragma unroll 4
@@ -545,20 +557,20 @@ __device__ __forceinline__ void tmem_ld16(u32 taddr, u32* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 // TMEM allocation by warp 0 (once per kernel); the base address lands in *slot.
-__device__ __forceinline__ u32 tmem_alloc(u32* slot, u32 ncols) {
+template <int NT> __device__ __forceinline__ u32 tmem_alloc(u32* slot, u32 ncols) {
   if ((threadIdx.x >> 5) == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  csync<NT>();
   tc_fence_after();
   return *(volatile u32*)slot;
 }
-__device__ __forceinline__ void tmem_free(u32 base, u32 ncols) {
+template <int NT> __device__ __forceinline__ void tmem_free(u32 base, u32 ncols) {
   tc_fence_before();
-  __syncthreads();
+  csync<NT>();
   if ((threadIdx.x >> 5) == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(ncols) : "memory");
 }
@@ -609,7 +621,7 @@ __device__ __forceinline__ void mm_gemv_tc(float* __restrict__ out, const float*
       for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    csync<NT>();
     auto issue = [&](int s) {
       const int kc = s / NTL, t = s % NTL;
       unsigned char* st = work + (s % S) * L::STAGE;
@@ -639,7 +651,7 @@ __device__ __forceinline__ void mm_gemv_tc(float* __restrict__ out, const float*
       }
       cp_async_wait<D>();
       fence_async_smem();
-      __syncthreads();
+      csync<NT>();
       if (tid == 0) {
         tc_fence_after();
         const int kc = s / NTL, t = s % NTL;
@@ -670,8 +682,254 @@ __device__ __forceinline__ void mm_gemv_tc(float* __restrict__ out, const float*
       }
     }
     tc_fence_before();
-    __syncthreads();
+    csync<NT>();
   }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed streaming of the large matmul operand (warp-specialised).
+//
+// A producer warp (one elected lane) walks the kernel's static sequence of
+// streamed boxes — every view operand of every streamed matmul, loop
+// iterations included — and issues cp.async.bulk.tensor loads into a ring of
+// S slots of SLOT bytes (full[s]: 1 arrival + tx bytes; empty[s]: consumer
+// release).  It runs ahead of the compute warps across node and loop
+// boundaries, so HBM streaming overlaps the candidate's elementwise, reduction
+// and cluster-flush phases.  Producer and consumers enumerate the same stage
+// sequence, each with its own running counter.
+
+constexpr int SLOT = 16384;
+
+__device__ __forceinline__ void mbar_expect_tx(u64* b, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const TmaDesc* tm, int c0, int c1, int c2, int c3, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"((u64)tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const TmaDesc* tm) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"((u64)tm) : "memory");
+}
+// producer: wait until slot (q % S) is free for its (q / S)-th fill
+template <int S> __device__ __forceinline__ u32 ring_acquire(u64* empty, u32 q) {
+  const u32 slot = q % S;
+  if (q >= (u32)S) mbar_wait(&empty[slot], ((q / S) - 1u) & 1u);
+  return slot;
+}
+// consumer: wait until the (q / S)-th fill of slot (q % S) has landed
+template <int S> __device__ __forceinline__ u32 ring_wait(u64* full, u32 q) {
+  const u32 slot = q % S;
+  mbar_wait(&full[slot], (q / S) & 1u);
+  return slot;
+}
+// UMMA smem descriptor, MN-major SWIZZLE_128B (layout type 2 on sm_100):
+// LBO = byte stride between 64-element MN atoms, SBO = stride between 8-row K groups.
+__device__ __forceinline__ u64 umma_desc_sw128(u32 saddr, u32 lbo, u32 sbo) {
+  return (u64)((saddr >> 4) & 0x3FFFu) | ((u64)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((u64)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// Streamed bf16 contraction on tcgen05:  out[b][m][n] = sum_k A[b][m][k] * B[b][k][n].
+// Stage (kc, t) = rows kc*KC.. of the 128-column tile t of B, as up to two TMA
+// boxes {64 n, KC k} (SWIZZLE_128B; box h at +h*KC*128 bytes).  Swap-AB: the B
+// tile is the MMA A operand (M = 128 columns, MN-major), A^T the MMA B operand
+// (N = 16, K-major, no swizzle; rows 8.. carry the bf16 residual of A when M <= 8).
+// Accumulators: TMEM columns t*16 .. t*16+15.  The MMA thread releases each slot
+// with tcgen05.commit on empty[slot] and signals `done` after the last stage.
+template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int NT>
+__device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const float* __restrict__ A,
+                                             unsigned char* __restrict__ xbuf, u32 tmem, unsigned char* ring, u64* full,
+                                             u64* empty, u64* done, u32& q, u32& dph) {
+  constexpr int NTL = (NN + 127) / 128;
+  constexpr int NKC = K / KC;
+  constexpr bool SPLIT = M <= 8;
+  constexpr u32 IDESC = UMMA_IDESC_BF16_M128_N16;
+  static_assert(K % KC == 0 && KC % 16 == 0 && KC * 256 <= SLOT && M <= 16 && NTL * 16 <= 512, "mm_stream_tc shape");
+  u16* xb = reinterpret_cast<u16*>(xbuf);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int bi = 0; bi < B0 * B1; ++bi) {
+    const int b1 = bi % B1, b0 = bi / B1;
+    const float* Ab = A + b0 * SA0 + b1 * SA1;
+    for (int e = tid; e < 16 * K; e += NT) {
+      const int kk = e & 7, m = (e >> 3) & 15, k = (e >> 7) * 8 + kk;
+      u16 v = 0;
+      if (m < M) {
+        v = NBF16::st(Ab[(i64)m * SA2 + (i64)k * SA3]);
+      } else if (SPLIT && m >= 8 && m - 8 < M) {
+        const float a = Ab[(i64)(m - 8) * SA2 + (i64)k * SA3];
+        v = NBF16::st(a - NBF16::ld(NBF16::st(a)));
+      }
+      xb[e] = v;
+    }
+    fence_async_smem();
+    csync<NT>();
+    const u32 q0 = q;
+    q += NKC * NTL;
+    if (tid == 0) {
+      const u32 xs = smem_u32(xb);
+#pragma unroll 1
+      for (int kc = 0; kc < NKC; ++kc) {
+#pragma unroll 1
+        for (int t = 0; t < NTL; ++t) {
+          const u32 slot = ring_wait<S>(full, q0 + (u32)(kc * NTL + t));
+          tc_fence_after();
+          const u32 st = smem_u32(ring + slot * SLOT);
+#pragma unroll
+          for (int ks = 0; ks < KC / 16; ++ks) {
+            const u64 ad = umma_desc_sw128(st + ks * 2048, KC * 128, 1024);
+            const u64 bd = umma_desc(xs + ((kc * KC + ks * 16) >> 3) * 256, 256, 128);
+            umma_bf16(tmem + t * 16, ad, bd, IDESC, (kc | ks) != 0);
+          }
+          umma_commit(&empty[slot]);
+        }
+      }
+      umma_commit(done);
+    }
+    mbar_wait(done, dph);
+    dph ^= 1u;
+    tc_fence_after();
+    for (int t = warp >> 2; t < NTL; t += NT / 128) {
+      u32 v[16];
+      tmem_ld16(tmem + ((u32)((warp & 3) * 32) << 16) + t * 16, v);
+      const int n = t * 128 + (warp & 3) * 32 + lane;
+      if (n < NN) {
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+          out[((i64)bi * M + m) * NN + n] = SPLIT ? __uint_as_float(v[m]) + __uint_as_float(v[8 + m])
+                                                  : __uint_as_float(v[m]);
+      }
+    }
+    tc_fence_before();
+    csync<NT>();
+  }
+}
+
+// Streamed fp32 contraction on CUDA cores.  Stage (t, kc) = one TMA box
+// {64 n, KC k} (no swizzle, row-major [KC][64]).  Thread layout: lane = cg + 8*kq
+// (cg: 8-column group, kq: 0..3), k-lane kl = warp*4 + kq strides the KC rows;
+// per k each thread reads 8 columns (2 x LDS.128) and A[k][0..M) (broadcast
+// within the 8 lanes of a k-lane), 8*M FMAs.  Partials reduce with shuffles over
+// kq, then across warps through `red` (NW*M*64 floats).  A thread owns columns
+// cg*4.. and 32+cg*4.. so each quarter-warp LDS.128 phase reads 128 contiguous
+// bytes (conflict-free); each warp's lane 0
+// releases the slot (empty count = NT/32).
+template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int NT>
+__device__ __forceinline__ void mm_stream_f32(float* __restrict__ out, const float* __restrict__ A,
+                                              float* __restrict__ at, float* __restrict__ red, unsigned char* ring,
+                                              u64* full, u64* empty, u32& q) {
+  constexpr int NT64 = (NN + 63) / 64;
+  constexpr int NKC = K / KC;
+  constexpr int NW = NT / 32;
+  constexpr int KL = NW * 4;
+  constexpr int A0 = SA0 ? B0 : 1, A1 = SA1 ? B1 : 1;
+  static_assert(K % KC == 0 && KC * 256 <= SLOT && M <= 8 && NT % 32 == 0, "mm_stream_f32 shape");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cg = lane & 7, kq = lane >> 3, kl = warp * 4 + kq;
+  // k-major copy of A: at[ab][k][m]
+  for (int e = tid; e < A0 * A1 * K * M; e += NT) {
+    const int m = e % M;
+    const int k = (e / M) % K;
+    const int ab = e / (M * K);
+    const int a1 = ab % A1, a0 = ab / A1;
+    at[e] = A[a0 * SA0 + a1 * SA1 + (i64)m * SA2 + (i64)k * SA3];
+  }
+  csync<NT>();
+  for (int bi = 0; bi < B0 * B1; ++bi) {
+    const int b1 = bi % B1, b0 = bi / B1;
+    const float* pa = at + (i64)((SA0 ? b0 : 0) * A1 + (SA1 ? b1 : 0)) * K * M;
+#pragma unroll 1
+    for (int t = 0; t < NT64; ++t) {
+      float acc[M][8];
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[m][v] = 0.0f;
+#pragma unroll 1
+      for (int kc = 0; kc < NKC; ++kc) {
+        const u32 slot = ring_wait<S>(full, q);
+        const float* st = reinterpret_cast<const float*>(ring + slot * SLOT);
+#pragma unroll 4
+        for (int k = kl; k < KC; k += KL) {
+          const float4 w0 = *reinterpret_cast<const float4*>(st + k * 64 + cg * 4);
+          const float4 w1 = *reinterpret_cast<const float4*>(st + k * 64 + 32 + cg * 4);
+          const float* ak = pa + (i64)(kc * KC + k) * M;
+          float av[M];
+          if constexpr (M % 4 == 0) {
+#pragma unroll
+            for (int u = 0; u < M / 4; ++u) *reinterpret_cast<float4*>(&av[u * 4]) = *reinterpret_cast<const float4*>(ak + u * 4);
+          } else {
+#pragma unroll
+            for (int m = 0; m < M; ++m) av[m] = ak[m];
+          }
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            acc[m][0] = fmaf(av[m], w0.x, acc[m][0]); acc[m][1] = fmaf(av[m], w0.y, acc[m][1]);
+            acc[m][2] = fmaf(av[m], w0.z, acc[m][2]); acc[m][3] = fmaf(av[m], w0.w, acc[m][3]);
+            acc[m][4] = fmaf(av[m], w1.x, acc[m][4]); acc[m][5] = fmaf(av[m], w1.y, acc[m][5]);
+            acc[m][6] = fmaf(av[m], w1.z, acc[m][6]); acc[m][7] = fmaf(av[m], w1.w, acc[m][7]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        ++q;
+      }
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          float x = acc[m][v];
+          x += __shfl_xor_sync(0xffffffffu, x, 8);
+          x += __shfl_xor_sync(0xffffffffu, x, 16);
+          acc[m][v] = x;
+        }
+      if (kq == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) red[(warp * M + m) * 64 + (v >> 2) * 32 + cg * 4 + (v & 3)] = acc[m][v];
+      }
+      csync<NT>();
+      for (int e = tid; e < M * 64; e += NT) {
+        const int m = e / 64, c = e % 64;
+        float x = 0.0f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) x += red[(w * M + m) * 64 + c];
+        const int n = t * 64 + c;
+        if (n < NN) out[((i64)bi * M + m) * NN + n] = x;
+      }
+      csync<NT>();
+    }
+  }
+}
+
+// Cluster barrier among compute threads only (the producer warp may be blocked
+// on its ring and must not be counted): thread 0 of every CTA arrives on every
+// peer's `bar` (count CL) with release.cluster and waits with acquire.cluster.
+template <int NT, int CL> __device__ __forceinline__ void cl_barrier(u64* bar, u32& phase) {
+  csync<NT>();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+#pragma unroll
+    for (u32 r = 0; r < (u32)CL; ++r) {
+      u32 remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(r));
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLAB_CW:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_CW;\n\tbra LAB_CW;\n\tDONE_CW:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+  }
+  phase ^= 1u;
+  csync<NT>();
 }
 
 // ---------------------------------------------------------------------------

@@ -33,11 +33,16 @@
 
 namespace sgm {
 // host mirror of sgm::Args in sgm_dev.cuh (kernel parameter block)
+struct alignas(64) TmaDesc {
+  uint64_t w[16];
+};
 struct Args {
   const void* in[16];
   void* out[16];
   void* scratch;
+  TmaDesc tm[4];
 };
+static_assert(sizeof(TmaDesc) == sizeof(CUtensorMap), "TmaDesc mirrors CUtensorMap");
 }  // namespace sgm
 
 namespace {
@@ -101,6 +106,9 @@ struct Driver {
   SGM_FN(cuGraphExecDestroy, CUgraphExec)
   SGM_FN(cuGraphDestroy, CUgraph)
   SGM_FN(cuOccupancyMaxActiveClusters, int*, CUfunction, const CUlaunchConfig*)
+  SGM_FN(cuTensorMapEncodeTiled, CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+         const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+         CUtensorMapL2promotion, CUtensorMapFloatOOBfill)
 #undef SGM_FN
   CUresult (*cuGetErrorString)(CUresult, const char**) = nullptr;
 
@@ -148,6 +156,7 @@ struct Driver {
     g &= sym(cuGraphLaunch, "cuGraphLaunch");
     g &= sym(cuGraphExecDestroy, "cuGraphExecDestroy");
     g &= sym(cuGraphDestroy, "cuGraphDestroy");
+    g &= sym(cuTensorMapEncodeTiled, "cuTensorMapEncodeTiled");
     sym(cuOccupancyMaxActiveClusters, "cuOccupancyMaxActiveClusters");
     sym(cuGetErrorString, "cuGetErrorString");
     ok = g;
@@ -306,6 +315,9 @@ struct sgm_plan {
   int64_t out_elems[SGM_MAX_SLOTS] = {0};
   double compile_ms = 0;
   int cache_hit = 0;
+  // TMA descriptors of the streamed operands, re-encoded when an input pointer changes
+  CUtensorMap tmaps[4];
+  const void* tmap_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
   CUstream tstream = nullptr;
 };
 
@@ -475,9 +487,36 @@ static int fill_nan(int ns, CUdeviceptr p, int64_t n, CUstream s) {
   return launch_1d(S.f_fill32, n, s, a);
 }
 
+static int encode_tmap(sgm_plan* p, int i, const void* ptr) {
+  const sgmcg::TmaSpec& t = p->gen.tmaps[i];
+  if (((uintptr_t)ptr & 15) != 0) return set_err(SGM_ERR_INVALID, "TMA operand (input slot %d) is not 16-byte aligned", t.slot);
+  cuuint64_t gdim[4] = {(cuuint64_t)t.dims[3], (cuuint64_t)t.dims[2], (cuuint64_t)t.dims[1], (cuuint64_t)t.dims[0]};
+  cuuint64_t es = (cuuint64_t)t.elem_bytes;
+  cuuint64_t gstride[3] = {gdim[0] * es, gdim[0] * gdim[1] * es, gdim[0] * gdim[1] * gdim[2] * es};
+  cuuint32_t box[4] = {(cuuint32_t)t.box0, (cuuint32_t)t.box1, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = D.cuTensorMapEncodeTiled(&p->tmaps[i],
+                                        t.elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                        4, const_cast<void*>(ptr), gdim, gstride, box, estr,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                        t.swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cu_check(r, "cuTensorMapEncodeTiled");
+  p->tmap_ptr[i] = ptr;
+  return SGM_OK;
+}
+
 static int launch_plan(sgm_plan* p, const void* const* inputs, void* const* outputs, CUstream s) {
   sgm::Args args;
   memset(&args, 0, sizeof args);
+  for (int i = 0; i < (int)p->gen.tmaps.size() && i < 4; ++i) {
+    const void* ptr = inputs[p->gen.tmaps[i].slot];
+    if (ptr != p->tmap_ptr[i]) {
+      int st = encode_tmap(p, i, ptr);
+      if (st) return st;
+    }
+    memcpy(&args.tm[i], &p->tmaps[i], sizeof(CUtensorMap));
+  }
   for (int k = 0; k < p->n_in; ++k) args.in[k] = inputs[k];
   for (int k = 0; k < p->n_out; ++k) args.out[k] = outputs[k];
   args.scratch = (void*)p->scratch;

@@ -124,6 +124,7 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.no_loop_split = int(h.get("no_loop_split", 0))
     d.hints.no_hoist = int(h.get("no_hoist", 0))
     d.hints.use_tcgen05 = int(h.get("use_tcgen05", 0))
+    d.hints.no_tma = int(h.get("no_tma", 0))
     return d
 
 
