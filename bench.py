@@ -236,7 +236,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference", "ours"])
     ap.add_argument("--workloads", default="R,G,A,Q,L")
-    ap.add_argument("--budget-us", type=float, default=1000.0, help="timing budget per candidate")
+    ap.add_argument("--budget-us", type=float, default=1000.0, help="(legacy) timing budget per candidate")
+    ap.add_argument("--refine-top", type=int, default=3, help="candidates per workload re-timed with 1000 launches")
     ap.add_argument("--best-iters", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -281,15 +282,17 @@ def main() -> None:
 
     log(f"{len(mine)}/{len(all_units)} candidates on this rank; compile+load {compile_s:.1f}s")
 
+    mine_by_w = {w: [u for u in mine if u.workload == w] for w in args.workloads}
+
     def step():
         recs = []
         t_w = {}
-        for u in mine:
+        for w in args.workloads:
             t0 = time.perf_counter()
-            recs.append(P.evaluate_unit(ctx[u.workload], u, budget_us=args.budget_us))
-            t_w[u.workload] = t_w.get(u.workload, 0.0) + time.perf_counter() - t0
+            recs.extend(P.evaluate_workload(ctx[w], mine_by_w[w], refine_top=args.refine_top))
+            t_w[w] = time.perf_counter() - t0
         errs = sum(1 for r in recs if r.error)
-        log("step " + " ".join(f"{w}:{t:.1f}s" for w, t in t_w.items()) + f" errors={errs}")
+        log("step " + " ".join(f"{w}:{t:.2f}s" for w, t in t_w.items()) + f" errors={errs}")
         for r in recs:
             if r.error:
                 log(f"  error {r.workload}#{r.index} {r.params} {r.error[:160]}")
@@ -345,29 +348,23 @@ def main() -> None:
     # ---- e2e: the same pass through the host-buffer C-ABI (H2D/D2H inside) ----
     e2e = None
     if not args.no_e2e:
-        host_ff = {w: [x.cpu().numpy() for x in ctx[w].ff_inputs] for w in args.workloads}
-        host_exp = {w: [x.cpu().numpy() for x in ctx[w].ff_expected] for w in args.workloads}
-        h2d = d2h = 0
+        # End to end through the public sweep API with HOST inputs: every step copies
+        # each workload's inputs (FF residues + one deployment-dtype set) from pinned
+        # host memory, evaluates the population, and reads verdicts + latencies back.
+        host = {w: [x.cpu().pin_memory() for x in ctx[w].ff_inputs + ctx[w].ws.sets[0]] for w in args.workloads}
+        h2d = sum(x.numel() * x.element_size() for w in args.workloads for x in host[w])
+        d2h = 0
 
         def e2e_step():
-            nonlocal h2d, d2h
-            h2d = d2h = 0
-            for u in mine:
-                c = ctx[u.workload]
-                try:
-                    plan = PLANS.get(u.cand, _abi.FF, None, local)
-                except Exception:
-                    continue
-                outs = [np.empty(tuple(c.program.spec(n).dims), dtype=np.int32) for n in c.program.outputs]
-                plan.run_host(host_ff[u.workload], outs)
-                h2d += sum(a.nbytes for a in host_ff[u.workload])
-                d2h += sum(a.nbytes for a in outs)
-                all(np.array_equal(a, b) for a, b in zip(outs, host_exp[u.workload]))
-                try:
-                    PLANS.get(u.cand, c.numsys, None, local).time(c.ws.sets, c.ws.outputs, warmup=1, iters=5)
-                except Exception:
-                    pass
-                d2h += 8
+            nonlocal d2h
+            d2h = 0
+            for w in args.workloads:
+                c = ctx[w]
+                for dst, src in zip(c.ff_inputs + c.ws.sets[0], host[w]):
+                    dst.copy_(src, non_blocking=True)
+                c.refresh_expected()  # the program's own FF run on the freshly copied inputs
+                rs = P.evaluate_workload(c, mine_by_w[w], refine_top=args.refine_top)
+                d2h += 16 * len(rs)  # mismatch counters + latencies
         e2e_step()
         torch.cuda.synchronize()
         barrier()
@@ -378,7 +375,7 @@ def main() -> None:
         f1.record()
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1)
-        log(f"e2e: {ems:.0f} ms/step, h2d {h2d / 1e9:.1f} GB")
+        log(f"e2e: {ems:.0f} ms/step, h2d {h2d / 1e9:.2f} GB")
         if dist is not None:
             t = torch.tensor([ems, h2d, d2h], dtype=torch.float64, device=f"cuda:{local}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -386,7 +383,8 @@ def main() -> None:
             h2d, d2h = int(t[1].item()) * world, int(t[2].item()) * world
         e2e = {"value": n_total / (ems / 1000.0), "unit": "candidates/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
-               "path": "sgm_plan_run_host (FF check with host numpy buffers) + sgm_plan_time per candidate"}
+               "path": "population.evaluate_workload (C-ABI sgm_plan_run / sgm_timer_*) with inputs copied from "
+                       "pinned host buffers and verdicts/latencies read back every step"}
 
     if rank != 0:
         if dist is not None:
@@ -440,7 +438,8 @@ def main() -> None:
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16/f32 timing + ff check", "data": "synthetic",
         "config": {"workload": "five-workload SIGMA population: " + ",".join(args.workloads),
-                   "candidates": n_total, "per_candidate": f"FF check + profile (~{args.budget_us:.0f}us budget)",
+                   "candidates": n_total, "per_candidate": "FF check (on-device mismatch count) + CUDA-event timing of one rotation of input "
+                                    f"sets; top {args.refine_top} per workload re-timed over 1000 launches",
                    "l2": "inputs rotated over sets totalling >= 3x L2 (cold L2 per launch)",
                    "compile_s_rank0": compile_s},
         "roofline": roof, "best_kernels": best, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),

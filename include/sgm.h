@@ -12,7 +12,7 @@
  *     (pkg/src/symfuse/interp.py:128-212)          (+ sgm_plan_run_host for host buffers)
  *   symfuse.interp.run_program                   sgm_plan_create(program-as-plan) + run
  *     (interp.py:69-83)
- *   symfuse.tuner.score_interp                   sgm_plan_time
+ *   symfuse.tuner.score_interp                   sgm_plan_time / sgm_timer_* (batched)
  *     (pkg/src/symfuse/tuner.py:160-174)
  *   symfuse.interp.random_equiv_test             sgm_ff_fill + sgm_plan_run (SGM_FF) +
  *     (interp.py:238-286)                          sgm_compare_u32 / sgm_rel_err
@@ -190,12 +190,28 @@ int sgm_plan_run_host(sgm_plan* plan, const void* const* host_inputs,
 int sgm_plan_time(sgm_plan* plan, const void* const* inputs, void* const* outputs,
                   int rot, int warmup, int iters, void* stream, double* mean_us);
 
+/* Batched, sync-free profiling of many plans (the candidate sweep).  Slot k
+ * times `reps` launches of a CUDA graph holding `rot` back-to-back launches (one
+ * per rotating input set; `inputs` = rot*n_inputs pointers), after one untimed
+ * warm-up launch of that graph, between two events recorded on `stream`.
+ * Nothing synchronises until sgm_timer_read, which waits for the last event and
+ * returns the mean microseconds per kernel launch of slots 0..n-1. */
+typedef struct sgm_timer sgm_timer;
+int sgm_timer_create(int capacity, sgm_timer** out);
+int sgm_timer_enqueue(sgm_timer* t, int slot, sgm_plan* plan, const void* const* inputs, void* const* outputs,
+                      int rot, int reps, void* stream);
+int sgm_timer_read(sgm_timer* t, int n, double* us_per_launch);
+int sgm_timer_destroy(sgm_timer* t);
+
 /* Counter-based uniform residues in [0, p): value(i) = mix64(key + i*G) mod p with
  * key = mix64(seed ^ mix64(salt)).  Same function as oracle/ff_np.py:ff_uniform. */
 int sgm_ff_fill(uint32_t* dst, int64_t n, uint64_t seed, uint64_t salt, void* stream);
 /* Number of positions where a != b (uint32). */
 int sgm_compare_u32(const uint32_t* a, const uint32_t* b, int64_t n, void* stream,
                     int64_t* mismatches);
+/* Asynchronous variant: adds the number of mismatching positions to
+ * *dev_counter (a device int64), no synchronisation. */
+int sgm_compare_u32_acc(const uint32_t* a, const uint32_t* b, int64_t n, void* stream, int64_t* dev_counter);
 /* rel_err(a, b) = max|a-b| / (1 + max|b|), +inf if a is non-finite (interp.py:228-231).
  * numsys selects the element type of both buffers (F64/F32/BF16). */
 int sgm_rel_err(const void* a, const void* b, int64_t n, int numsys, void* stream,

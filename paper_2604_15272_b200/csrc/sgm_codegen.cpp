@@ -787,7 +787,9 @@ struct Gen {
         // TMA-fed streaming (producer warp + ring): bf16 on tcgen05, fp32 on CUDA cores
         x.tma = false;
         const i64 d3 = in_dims[b.slot][3];
-        const bool batch_ok = x.sl[0] * x.sl[1] <= 8 && b.sl[3] == NN && b.sl[2] == K;
+        // every box starts 16-byte aligned iff the slice width along n is a multiple of 16 bytes
+        // (all start terms are multiples of it); TMA faults on misaligned box starts
+        const bool batch_ok = x.sl[0] * x.sl[1] <= 8 && b.sl[3] == NN && b.sl[2] == K && (NN * es) % 16 == 0;
         if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 && (ns == SGM_BF16 || ns == SGM_F32)) {
           if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && (d3 * 2) % 16 == 0 &&
               ntl * 16 <= 512) {

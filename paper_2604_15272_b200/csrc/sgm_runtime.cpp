@@ -319,6 +319,19 @@ struct sgm_plan {
   CUtensorMap tmaps[4];
   const void* tmap_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
   CUstream tstream = nullptr;
+  // cached CUDA graph of `graph_rot` launches over one rotation of input sets
+  CUgraph graph = nullptr;
+  CUgraphExec gexec = nullptr;
+  std::vector<const void*> graph_key;
+  int graph_rot = 0;
+};
+
+struct sgm_timer {
+  int cap = 0;
+  int device = 0;
+  std::vector<CUevent> ev;      // 2 per slot
+  std::vector<int> launches;    // kernel launches timed in each slot
+  int last = -1;
 };
 
 extern "C" {
@@ -461,11 +474,13 @@ int sgm_plan_source(const sgm_plan* p, char* buf, size_t cap, size_t* len) {
 
 int sgm_plan_destroy(sgm_plan* p) {
   if (!p) return SGM_OK;
-  if (p->mod || p->scratch || p->tstream) {
+  if (p->mod || p->scratch || p->tstream || p->gexec || p->graph) {
     if (D.ok && p->device >= 0 && g_dev[p->device].init) D.cuCtxSetCurrent(g_dev[p->device].ctx);
     if (p->mod) D.cuModuleUnload(p->mod);
     if (p->scratch) D.cuMemFree(p->scratch);
     if (p->tstream) D.cuStreamDestroy(p->tstream);
+    if (p->gexec) D.cuGraphExecDestroy(p->gexec);
+    if (p->graph) D.cuGraphDestroy(p->graph);
   }
   delete p;
   return SGM_OK;
@@ -589,6 +604,8 @@ int sgm_plan_run_host(sgm_plan* p, const void* const* host_inputs, void* const* 
   return SGM_OK;
 }
 
+static int plan_graph(sgm_plan* p, const void* const* inputs, void* const* outputs, int rot);
+
 int sgm_plan_time(sgm_plan* p, const void* const* inputs, void* const* outputs, int rot, int warmup, int iters,
                   void* stream, double* mean_us) {
   if (!p || !p->fn || !mean_us) return set_err(SGM_ERR_INVALID, "null plan / no device");
@@ -596,47 +613,118 @@ int sgm_plan_time(sgm_plan* p, const void* const* inputs, void* const* outputs, 
   if (st) return st;
   if (rot < 1) rot = 1;
   if (iters < 1) iters = 1;
-  if (!p->tstream) CU(D.cuStreamCreate(&p->tstream, CU_STREAM_NON_BLOCKING));
-  CUstream s = p->tstream;
   CUstream user = (CUstream)stream;
   if (user) CU(D.cuStreamSynchronize(user));
+  if ((st = plan_graph(p, inputs, outputs, rot))) return st;
+  CUstream s = p->tstream;
   for (int w = 0; w < warmup; ++w)
     if ((st = launch_plan(p, inputs + (size_t)(w % rot) * p->n_in, outputs, s))) return st;
-  // capture `iters` launches into one graph (launch overhead off the critical path)
-  CUgraph g = nullptr;
-  CUgraphExec ge = nullptr;
-  bool graph_ok = D.cuStreamBeginCapture(s, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL) == CUDA_SUCCESS;
-  if (graph_ok) {
-    for (int i = 0; i < iters; ++i) {
-      if (launch_plan(p, inputs + (size_t)(i % rot) * p->n_in, outputs, s)) { graph_ok = false; break; }
-    }
-    CUresult r = D.cuStreamEndCapture(s, &g);
-    graph_ok = graph_ok && r == CUDA_SUCCESS && g;
-    if (graph_ok) graph_ok = D.cuGraphInstantiateWithFlags(&ge, g, 0) == CUDA_SUCCESS;
-  }
+  const int reps = (iters + rot - 1) / rot;
   CUevent e0, e1;
   CU(D.cuEventCreate(&e0, 0));
   CU(D.cuEventCreate(&e1, 0));
-  if (graph_ok) { CU(D.cuGraphLaunch(ge, s)); g_launches += iters; }  // warm the graph once
-  CU(D.cuStreamSynchronize(s));
+  CU(D.cuGraphLaunch(p->gexec, s));  // warm the graph once
   CU(D.cuEventRecord(e0, s));
-  if (graph_ok) {
-    CU(D.cuGraphLaunch(ge, s));
-    g_launches += iters;
-  } else {
-    for (int i = 0; i < iters; ++i)
-      if ((st = launch_plan(p, inputs + (size_t)(i % rot) * p->n_in, outputs, s))) return st;
-  }
+  for (int r = 0; r < reps; ++r) CU(D.cuGraphLaunch(p->gexec, s));
   CU(D.cuEventRecord(e1, s));
   CU(D.cuEventSynchronize(e1));
+  g_launches += (long long)rot * (reps + 1);
   float ms = 0;
   CU(D.cuEventElapsedTime(&ms, e0, e1));
-  *mean_us = (double)ms * 1000.0 / iters;
+  *mean_us = (double)ms * 1000.0 / ((double)reps * rot);
   D.cuEventDestroy(e0);
   D.cuEventDestroy(e1);
-  if (ge) D.cuGraphExecDestroy(ge);
-  if (g) D.cuGraphDestroy(g);
   return SGM_OK;
+}
+
+// (Re)build the plan's cached graph: `rot` launches, launch i reading input set i.
+static int plan_graph(sgm_plan* p, const void* const* inputs, void* const* outputs, int rot) {
+  std::vector<const void*> key(inputs, inputs + (size_t)rot * p->n_in);
+  key.insert(key.end(), outputs, outputs + p->n_out);
+  if (p->gexec && p->graph_rot == rot && key == p->graph_key) return SGM_OK;
+  if (p->gexec) { D.cuGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+  if (p->graph) { D.cuGraphDestroy(p->graph); p->graph = nullptr; }
+  if (!p->tstream) CU(D.cuStreamCreate(&p->tstream, CU_STREAM_NON_BLOCKING));
+  CU(D.cuStreamBeginCapture(p->tstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
+  int st = SGM_OK;
+  for (int i = 0; i < rot && !st; ++i) st = launch_plan(p, inputs + (size_t)i * p->n_in, outputs, p->tstream);
+  CUgraph g = nullptr;
+  CUresult r = D.cuStreamEndCapture(p->tstream, &g);
+  if (st) { if (g) D.cuGraphDestroy(g); return st; }
+  if (r != CUDA_SUCCESS) return cu_check(r, "cuStreamEndCapture");
+  r = D.cuGraphInstantiateWithFlags(&p->gexec, g, 0);
+  if (r != CUDA_SUCCESS) { D.cuGraphDestroy(g); return cu_check(r, "cuGraphInstantiate"); }
+  p->graph = g;
+  p->graph_key = key;
+  p->graph_rot = rot;
+  return SGM_OK;
+}
+
+int sgm_timer_create(int capacity, sgm_timer** out) {
+  int st = ensure_ctx();
+  if (st) return st;
+  if (capacity < 1 || !out) return set_err(SGM_ERR_INVALID, "bad timer capacity");
+  sgm_timer* t = new sgm_timer();
+  t->cap = capacity;
+  t->device = t_device;
+  t->ev.resize((size_t)capacity * 2, nullptr);
+  t->launches.assign(capacity, 0);
+  for (auto& e : t->ev) {
+    CUresult r = D.cuEventCreate(&e, 0);
+    if (r != CUDA_SUCCESS) { sgm_timer_destroy(t); return cu_check(r, "cuEventCreate"); }
+  }
+  *out = t;
+  return SGM_OK;
+}
+
+int sgm_timer_enqueue(sgm_timer* t, int slot, sgm_plan* p, const void* const* inputs, void* const* outputs, int rot,
+                      int reps, void* stream) {
+  if (!t || !p || !p->fn || slot < 0 || slot >= t->cap) return set_err(SGM_ERR_INVALID, "bad timer / plan / slot");
+  int st = ensure_ctx();
+  if (st) return st;
+  if (rot < 1) rot = 1;
+  if (reps < 1) reps = 1;
+  if ((st = plan_graph(p, inputs, outputs, rot))) return st;
+  CUstream s = (CUstream)stream;
+  CU(D.cuGraphLaunch(p->gexec, s));  // warm-up (instruction cache, TMA descriptors)
+  CU(D.cuEventRecord(t->ev[2 * slot], s));
+  for (int r = 0; r < reps; ++r) CU(D.cuGraphLaunch(p->gexec, s));
+  CU(D.cuEventRecord(t->ev[2 * slot + 1], s));
+  g_launches += (long long)rot * (reps + 1);
+  t->launches[slot] = rot * reps;
+  if (slot > t->last) t->last = slot;
+  return SGM_OK;
+}
+
+int sgm_timer_read(sgm_timer* t, int n, double* us) {
+  if (!t || !us || n < 0 || n > t->cap) return set_err(SGM_ERR_INVALID, "bad timer read");
+  int st = ensure_ctx();
+  if (st) return st;
+  for (int k = 0; k < n; ++k) {
+    if (!t->launches[k]) { us[k] = -1.0; continue; }
+    CU(D.cuEventSynchronize(t->ev[2 * k + 1]));
+    float ms = 0;
+    CU(D.cuEventElapsedTime(&ms, t->ev[2 * k], t->ev[2 * k + 1]));
+    us[k] = (double)ms * 1000.0 / t->launches[k];
+  }
+  return SGM_OK;
+}
+
+int sgm_timer_destroy(sgm_timer* t) {
+  if (!t) return SGM_OK;
+  for (auto e : t->ev)
+    if (e) D.cuEventDestroy(e);
+  delete t;
+  return SGM_OK;
+}
+
+int sgm_compare_u32_acc(const uint32_t* a, const uint32_t* b, int64_t n, void* stream, int64_t* dev_counter) {
+  int st = ensure_ctx();
+  if (st) return st;
+  DevState& S = g_dev[t_device];
+  CUdeviceptr pa = (CUdeviceptr)a, pb = (CUdeviceptr)b, pc = (CUdeviceptr)dev_counter;
+  void* args[] = {&pa, &pb, &n, &pc};
+  return launch_1d(S.f_cmp, n, (CUstream)stream, args);
 }
 
 int sgm_ff_fill(uint32_t* dst, int64_t n, uint64_t seed, uint64_t salt, void* stream) {

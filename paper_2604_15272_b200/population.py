@@ -166,6 +166,7 @@ class Record:
     error: Optional[str] = None
     plan: dict = field(default_factory=dict)
     pruned: bool = False
+    refined: bool = False
 
 
 class WorkloadContext:
@@ -186,7 +187,15 @@ class WorkloadContext:
             seed64 = ff_trial_seed(seed, 0x5EED0000 + WORKLOADS.index(self.name) if self.name in WORKLOADS else 0, 0)
             self.ff_inputs = ff_fill_inputs(self.program, seed64, device)
             self.ff_expected = ff_run(ir.program_candidate(self.program), self.ff_inputs, device)
+            self.ff_out = [torch().empty_like(x) for x in self.ff_expected]
         self.bytes = algorithmic_bytes(pop)
+
+    def refresh_expected(self) -> None:
+        """Re-run the program in GF(p) on the current FF inputs (into ff_expected)."""
+        from .ff import ff_run
+        outs = ff_run(ir.program_candidate(self.program), self.ff_inputs, self.device)
+        for dst, src in zip(self.ff_expected, outs):
+            dst.copy_(src)
         self.best_us = None  # running best latency (prunes precise timing of losers)
 
 
@@ -213,6 +222,105 @@ def evaluate_unit(ctx: WorkloadContext, u: Unit, budget_us: float = 2000.0, max_
     except Exception as exc:
         rec.error = f"{type(exc).__name__}: {str(exc)[:300]}"
     return rec
+
+
+class Timer:
+    """Batched, sync-free CUDA-event profiling (libsgm sgm_timer_*)."""
+
+    def __init__(self, capacity: int, device: int):
+        import ctypes as C
+        _abi.bind_device(device)
+        self.cap = max(1, capacity)
+        self.device = device
+        h = C.c_void_p()
+        _abi.check(_abi.lib().sgm_timer_create(self.cap, C.byref(h)))
+        self._h = h
+
+    def enqueue(self, slot: int, plan: Plan, input_sets, outputs, reps: int = 1) -> None:
+        import ctypes as C
+        ip = _abi.ptr_array([t.data_ptr() for ins in input_sets for t in ins])
+        op = _abi.ptr_array([t.data_ptr() for t in outputs])
+        s = torch().cuda.current_stream(self.device).cuda_stream
+        _abi.check(_abi.lib().sgm_timer_enqueue(self._h, slot, plan._h, ip, op, len(input_sets), reps, C.c_void_p(s)))
+
+    def read(self, n: int) -> list:
+        import ctypes as C
+        out = (C.c_double * max(1, n))()
+        _abi.check(_abi.lib().sgm_timer_read(self._h, n, out))
+        return [out[k] for k in range(n)]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _abi.lib().sgm_timer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_reps: int = 1,
+                      refine_top: int = 3, refine_launches: int = 1000) -> list:
+    """Evaluate candidates of one workload with no per-candidate host synchronisation.
+
+    Pass 1 enqueues, per candidate, the finite-field run (outputs NaN-filled
+    first) + an on-device mismatch count against the program's FF output, and a
+    timed CUDA graph of one rotation over the input sets (after a warm-up
+    launch).  One read at the end collects verdicts and latencies.  Pass 2
+    re-times the `refine_top` fastest FF-equivalent candidates with
+    `refine_launches` launches (the paper's 1000-run protocol)."""
+    import ctypes as C
+    t = torch()
+    dev = ctx.device
+    n = len(us)
+    recs = [Record(u.workload, u.index, u.pair, dict(u.cand.params), u.cand.mapping_list()) for u in us]
+    if n == 0:
+        return recs
+    counters = t.zeros(n, dtype=t.int64, device=dev)
+    stream = C.c_void_p(t.cuda.current_stream(dev).cuda_stream)
+    L = _abi.lib()
+    timer = Timer(n, dev)
+    for k, u in enumerate(us):
+        rec = recs[k]
+        try:
+            if ff:
+                PLANS.get(u.cand, _abi.FF, None, dev).run(ctx.ff_inputs, ctx.ff_out)
+                for g, e in zip(ctx.ff_out, ctx.ff_expected):
+                    _abi.check(L.sgm_compare_u32_acc(C.c_void_p(g.data_ptr()), C.c_void_p(e.data_ptr()), g.numel(),
+                                                     stream, C.c_void_p(counters.data_ptr() + 8 * k)))
+            plan = PLANS.get(u.cand, ctx.numsys, None, dev)
+            timer.enqueue(k, plan, ctx.ws.sets, ctx.ws.outputs, reps=screen_reps)
+            rec.plan = {x: plan.info[x] for x in ("ctas", "cluster", "smem_bytes", "free_parts", "loop_parts",
+                                                  "kernel_name", "summary")}
+        except Exception as exc:  # recorded, the sweep goes on (SURVEY §5: failures are reported)
+            rec.error = f"{type(exc).__name__}: {str(exc)[:300]}"
+    lat = timer.read(n)
+    mism = counters.cpu().tolist()
+    timer.close()
+    for k, rec in enumerate(recs):
+        if rec.error is None:
+            rec.latency_us = lat[k] if lat[k] >= 0 else None
+            rec.ff_ok = (mism[k] == 0) if ff else None
+    ok = sorted((r for r in recs if r.error is None and r.latency_us is not None and r.ff_ok is not False),
+                key=lambda r: (r.latency_us, r.index))
+    top = ok[:refine_top]
+    if top:
+        timer = Timer(len(top), dev)
+        pos = {r.index: k for k, r in enumerate(recs)}
+        for j, r in enumerate(top):
+            plan = PLANS.get(us[pos[r.index]].cand, ctx.numsys, None, dev)
+            timer.enqueue(j, plan, ctx.ws.sets, ctx.ws.outputs, reps=max(1, -(-refine_launches // ctx.ws.rot)))
+        lat2 = timer.read(len(top))
+        timer.close()
+        for j, r in enumerate(top):
+            r.latency_us = lat2[j]
+            r.refined = True
+    for r in recs:
+        if r.latency_us is not None and not r.refined:
+            r.pruned = True  # screening measurement only (one rotation)
+    return recs
 
 
 def argmin(records: list) -> Optional[Record]:

@@ -1,0 +1,55 @@
+"""The batched candidate sweep on the B200 (population.evaluate_workload):
+on-device FF verdicts agree with per-candidate checks, mutated (wrong)
+candidates are refuted, and the profiler's latencies are sane."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    import paper_2604_15272_b200 as S
+    return S
+
+
+@pytest.mark.parametrize("w,k", [("R", 12), ("L", 16), ("A", 16)])
+def test_sweep_verdicts_and_latencies(S, w, k):
+    from paper_2604_15272_b200 import population as P
+    pop = P.load_population(w)
+    us = P.units(pop)
+    us = us[:: max(1, len(us) // k)][:k]
+    ctx = P.WorkloadContext(pop, 0)
+    recs = P.evaluate_workload(ctx, us, refine_top=2, refine_launches=64)
+    assert all(r.error is None for r in recs), [r.error for r in recs if r.error]
+    assert all(r.ff_ok for r in recs)
+    lat = [r.latency_us for r in recs]
+    assert all(x is not None and 0.5 < x < 1e5 for x in lat), lat
+    assert sum(r.refined for r in recs) == 2
+    # the batched verdicts equal the per-candidate path
+    for u, r in list(zip(us, recs))[:4]:
+        one = P.evaluate_unit(ctx, u, budget_us=100.0)
+        assert one.ff_ok == r.ff_ok
+
+
+def test_sweep_refutes_a_wrong_candidate(S):
+    """A candidate whose saver map drops a grid dim writes only some cells:
+    the sweep's FF check must refute it (or the plan must raise)."""
+    from paper_2604_15272_b200 import ir
+    from paper_2604_15272_b200 import population as P
+    pop = P.load_population("R")
+    prog = ir.Program.from_json(pop["program"])
+    c = pop["candidates"][0]
+    good = ir.from_serialized(c["key"], prog, c["space"][3])
+    # swap which operand the grid splits: W columns split but O rows split -> wrong results
+    bad_map = frozenset({("W", 1, "x"), ("O", 0, "x")})
+    bad = ir.Candidate(prog, good.block, bad_map, dict(good.params))
+    u_good = P.Unit(0, "R", 0, good)
+    u_bad = P.Unit(1, "R", 0, bad)
+    ctx = P.WorkloadContext(pop, 0)
+    recs = P.evaluate_workload(ctx, [u_good, u_bad], refine_top=1, refine_launches=16)
+    assert recs[0].ff_ok is True
+    assert recs[1].error is not None or recs[1].ff_ok is False
