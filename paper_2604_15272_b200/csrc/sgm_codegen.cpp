@@ -1106,6 +1106,8 @@ struct Gen {
 
   void emit_producer() {
     os << "    if (tid == NT) {\n      unsigned pq = 0;\n";
+    os << "      for (long long item = cid; item < " << LB * FP << "LL; item += ncl) {\n";
+    emit_item_vars("      ");
     bool in_loop = false;
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
@@ -1119,7 +1121,7 @@ struct Gen {
         emit_producer_node(e.node, in_loop);
       }
     }
-    os << "    }\n    return;\n";
+    os << "      }\n    }\n    return;\n";
   }
 
   // vector width for a loader (x) or a saver (x = saver node, sl = its input's slice)
@@ -1317,6 +1319,21 @@ struct Gen {
     os << "    sgm::csync<NT>();\n";
   }
 
+  // per-item coordinates: free part, grid coordinates, free-part split indices
+  void emit_item_vars(const char* ind) {
+    static const char* gv[3] = {"gx", "gy", "gz"};
+    os << ind << "long long rest = item;\n";
+    os << ind << "const long long fpart = rest % " << FP << "; rest /= " << FP << "; (void)fpart;\n";
+    for (int g = 0; g < ngrid; ++g)
+      os << ind << "const long long " << gv[g] << " = rest % " << grid[g] << "; rest /= " << grid[g] << "; (void)"
+         << gv[g] << ";\n";
+    for (int c = 0; c < (int)cls.size(); ++c) {
+      if (cls[c].parts <= 1 || cls[c].cluster) continue;
+      os << ind << "const int " << part_var(c) << " = (int)((fpart / " << cls[c].radix << "LL) % " << cls[c].parts
+         << "LL);\n";
+    }
+  }
+
   void emit() {
     os << "#include \"sgm_dev.cuh\"\n";
     os << "// generated by sgm_codegen.cpp: logical blocks " << LB << ", free parts " << FP << ", cluster " << CL
@@ -1331,20 +1348,13 @@ struct Gen {
     os << "  const long long bid = blockIdx.x;\n";
     if (CL > 1) os << "  const unsigned crank = sgm::cluster_rank();\n";
     else os << "  const unsigned crank = 0u; (void)crank;\n";
-    os << "  long long rest = bid / " << CL << ";\n";
-    os << "  const long long fpart = rest % " << FP << "; rest /= " << FP << "; (void)fpart;\n";
-    static const char* gv[3] = {"gx", "gy", "gz"};
-    for (int g = 0; g < ngrid; ++g)
-      os << "  const long long " << gv[g] << " = rest % " << grid[g] << "; rest /= " << grid[g] << "; (void)" << gv[g]
-         << ";\n";
+    // persistent: cluster `cid` of `ncl` processes work items cid, cid + ncl, ... (item = logical
+    // block x free part); the cluster-split parts and loop part are fixed per CTA
+    os << "  const long long cid = bid / " << CL << ", ncl = (long long)gridDim.x / " << CL << ";\n";
     for (int c = 0; c < (int)cls.size(); ++c) {
-      if (cls[c].parts <= 1) continue;
-      if (cls[c].cluster)
-        os << "  const int " << part_var(c) << " = (int)((crank >> " << cls[c].bit_shift << ") & " << (cls[c].parts - 1)
-           << "u);\n";
-      else
-        os << "  const int " << part_var(c) << " = (int)((fpart / " << cls[c].radix << "LL) % " << cls[c].parts
-           << "LL);\n";
+      if (cls[c].parts <= 1 || !cls[c].cluster) continue;
+      os << "  const int " << part_var(c) << " = (int)((crank >> " << cls[c].bit_shift << ") & " << (cls[c].parts - 1)
+         << "u);\n";
     }
     if (LP > 1) os << "  const int jp = (int)((crank >> " << loop_shift << ") & " << (LP - 1) << "u);\n";
     else os << "  const int jp = 0; (void)jp;\n";
@@ -1390,6 +1400,8 @@ struct Gen {
       os << "  __shared__ unsigned tmem_slot;\n";
       os << "  const unsigned tmem_base = sgm::tmem_alloc<NT>(&tmem_slot, " << tmem_cols << "u);\n";
     }
+    os << "  for (long long item = cid; item < " << LB * FP << "LL; item += ncl) {\n";
+    emit_item_vars("  ");
     bool in_loop = false;
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
@@ -1409,6 +1421,7 @@ struct Gen {
         emit_node(e.node, in_loop);
       }
     }
+    os << "  sgm::csync<NT>();  // tiles are reused by the next item\n  }\n";
     if (tmem_cols) os << "  sgm::tmem_free<NT>(tmem_base, " << tmem_cols << "u);\n";
     os << "}\n";
   }

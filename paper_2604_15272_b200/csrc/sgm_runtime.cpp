@@ -106,6 +106,7 @@ struct Driver {
   SGM_FN(cuGraphExecDestroy, CUgraphExec)
   SGM_FN(cuGraphDestroy, CUgraph)
   SGM_FN(cuOccupancyMaxActiveClusters, int*, CUfunction, const CUlaunchConfig*)
+  SGM_FN(cuOccupancyMaxActiveBlocksPerMultiprocessor, int*, CUfunction, int, size_t)
   SGM_FN(cuTensorMapEncodeTiled, CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
          CUtensorMapL2promotion, CUtensorMapFloatOOBfill)
@@ -158,6 +159,7 @@ struct Driver {
     g &= sym(cuGraphDestroy, "cuGraphDestroy");
     g &= sym(cuTensorMapEncodeTiled, "cuTensorMapEncodeTiled");
     sym(cuOccupancyMaxActiveClusters, "cuOccupancyMaxActiveClusters");
+    sym(cuOccupancyMaxActiveBlocksPerMultiprocessor, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     sym(cuGetErrorString, "cuGetErrorString");
     ok = g;
     return ok;
@@ -270,6 +272,10 @@ int compile_cubin(const std::string& src, std::string& cubin, double& ms, int& h
     std::string log(ls, '\0');
     nvrtcGetProgramLog(prog, &log[0]);
     nvrtcDestroyProgram(&prog);
+    if (const char* dump = getenv("SGM_DUMP_FAILED")) {  // debugging aid: keep the failing source
+      std::ofstream f(dump);
+      f << src;
+    }
     if (log.size() > 1800) log = log.substr(0, 1800);
     return set_err(SGM_ERR_NVRTC, "NVRTC: %s\n%s", nvrtcGetErrorString(r), log.c_str());
   }
@@ -309,6 +315,7 @@ struct sgm_plan {
   CUfunction fn = nullptr;
   CUdeviceptr scratch = 0;
   int numsys = 0;
+  int64_t launch_ctas = 0;   // persistent grid: min(work CTAs, co-resident CTAs)
   int n_in = 0, n_out = 0;
   size_t in_bytes[SGM_MAX_SLOTS] = {0};
   size_t out_bytes[SGM_MAX_SLOTS] = {0};
@@ -433,6 +440,37 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
     r = D.cuFuncSetAttribute(p->fn, CU_FUNC_ATTRIBUTE_NON_PORTABLE_CLUSTER_SIZE_ALLOWED, 1);
     if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuFuncSetAttribute(cluster)"); }
   }
+  {
+    // persistent launch: at most the CTAs (whole clusters) that can be co-resident
+    int64_t resident = 0;
+    if (gr.cluster > 1 && D.cuOccupancyMaxActiveClusters) {
+      CUlaunchAttribute attr;
+      memset(&attr, 0, sizeof attr);
+      attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+      attr.value.clusterDim.x = (unsigned)gr.cluster;
+      attr.value.clusterDim.y = 1;
+      attr.value.clusterDim.z = 1;
+      CUlaunchConfig cfg;
+      memset(&cfg, 0, sizeof cfg);
+      cfg.gridDimX = (unsigned)gr.ctas;
+      cfg.gridDimY = cfg.gridDimZ = 1;
+      cfg.blockDimX = (unsigned)gr.threads;
+      cfg.blockDimY = cfg.blockDimZ = 1;
+      cfg.sharedMemBytes = (unsigned)gr.smem_bytes;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (D.cuOccupancyMaxActiveClusters(&ncl, p->fn, &cfg) == CUDA_SUCCESS && ncl > 0) resident = (int64_t)ncl * gr.cluster;
+    } else if (gr.cluster == 1 && D.cuOccupancyMaxActiveBlocksPerMultiprocessor) {
+      int nb = 0;
+      if (D.cuOccupancyMaxActiveBlocksPerMultiprocessor(&nb, p->fn, gr.threads, (size_t)gr.smem_bytes) == CUDA_SUCCESS &&
+          nb > 0)
+        resident = (int64_t)nb * g_dev[t_device].sms;
+    }
+    p->launch_ctas = gr.ctas;
+    if (resident > 0 && resident < gr.ctas) p->launch_ctas = resident / gr.cluster * gr.cluster;
+    if (p->launch_ctas < gr.cluster) p->launch_ctas = gr.cluster;
+  }
   if (gr.scratch_bytes > 0) {
     r = D.cuMemAlloc(&p->scratch, (size_t)gr.scratch_bytes);
     if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuMemAlloc(scratch)"); }
@@ -457,7 +495,8 @@ int sgm_plan_info_get(const sgm_plan* p, sgm_plan_info* info) {
   info->n_tcgen05 = p->gen.n_tcgen05;
   info->source_hash = sgmcg::fnv1a(p->gen.source);
   snprintf(info->kernel_name, sizeof info->kernel_name, "%s", p->gen.kernel_name.c_str());
-  snprintf(info->plan_summary, sizeof info->plan_summary, "%s", p->gen.summary.c_str());
+  snprintf(info->plan_summary, sizeof info->plan_summary, "grid=%lld %s", (long long)p->launch_ctas,
+           p->gen.summary.c_str());
   return SGM_OK;
 }
 
@@ -536,7 +575,7 @@ static int launch_plan(sgm_plan* p, const void* const* inputs, void* const* outp
   for (int k = 0; k < p->n_out; ++k) args.out[k] = outputs[k];
   args.scratch = (void*)p->scratch;
   void* params[] = {&args};
-  CU(D.cuLaunchKernel(p->fn, (unsigned)p->gen.ctas, 1, 1, (unsigned)p->gen.threads, 1, 1,
+  CU(D.cuLaunchKernel(p->fn, (unsigned)p->launch_ctas, 1, 1, (unsigned)p->gen.threads, 1, 1,
                       (unsigned)p->gen.smem_bytes, s, params, nullptr));
   g_launches++;  // during graph capture this counts the captured node once
   return SGM_OK;

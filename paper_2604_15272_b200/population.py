@@ -167,6 +167,7 @@ class Record:
     plan: dict = field(default_factory=dict)
     pruned: bool = False
     refined: bool = False
+    timing: str = ""
 
 
 class WorkloadContext:
@@ -261,16 +262,17 @@ class Timer:
             pass
 
 
-def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_reps: int = 1,
+def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_factor: float = 2.0,
                       refine_top: int = 3, refine_launches: int = 1000) -> list:
     """Evaluate candidates of one workload with no per-candidate host synchronisation.
 
     Pass 1 enqueues, per candidate, the finite-field run (outputs NaN-filled
-    first) + an on-device mismatch count against the program's FF output, and a
-    timed CUDA graph of one rotation over the input sets (after a warm-up
-    launch).  One read at the end collects verdicts and latencies.  Pass 2
-    re-times the `refine_top` fastest FF-equivalent candidates with
-    `refine_launches` launches (the paper's 1000-run protocol)."""
+    first) + an on-device mismatch count against the program's FF output, and one
+    timed launch (after one untimed launch, on its own input set, so it streams
+    from HBM).  Pass 2 times one full rotation over the input sets (each launch
+    misses L2) for the candidates within `screen_factor` of the pass-1 best.
+    Pass 3 re-times the `refine_top` fastest with `refine_launches` launches (the
+    paper's 1000-run protocol).  One host read per pass."""
     import ctypes as C
     t = torch()
     dev = ctx.device
@@ -281,6 +283,8 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
     counters = t.zeros(n, dtype=t.int64, device=dev)
     stream = C.c_void_p(t.cuda.current_stream(dev).cuda_stream)
     L = _abi.lib()
+    rot = ctx.ws.rot
+    plans = [None] * n
     timer = Timer(n, dev)
     for k, u in enumerate(us):
         rec = recs[k]
@@ -290,8 +294,8 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
                 for g, e in zip(ctx.ff_out, ctx.ff_expected):
                     _abi.check(L.sgm_compare_u32_acc(C.c_void_p(g.data_ptr()), C.c_void_p(e.data_ptr()), g.numel(),
                                                      stream, C.c_void_p(counters.data_ptr() + 8 * k)))
-            plan = PLANS.get(u.cand, ctx.numsys, None, dev)
-            timer.enqueue(k, plan, ctx.ws.sets, ctx.ws.outputs, reps=screen_reps)
+            plan = plans[k] = PLANS.get(u.cand, ctx.numsys, None, dev)
+            timer.enqueue(k, plan, [ctx.ws.sets[k % rot]], ctx.ws.outputs, reps=1)
             rec.plan = {x: plan.info[x] for x in ("ctas", "cluster", "smem_bytes", "free_parts", "loop_parts",
                                                   "kernel_name", "summary")}
         except Exception as exc:  # recorded, the sweep goes on (failures are reported)
@@ -303,23 +307,33 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
         if rec.error is None:
             rec.latency_us = lat[k] if lat[k] >= 0 else None
             rec.ff_ok = (mism[k] == 0) if ff else None
-    ok = sorted((r for r in recs if r.error is None and r.latency_us is not None and r.ff_ok is not False),
-                key=lambda r: (r.latency_us, r.index))
-    top = ok[:refine_top]
-    if top:
-        timer = Timer(len(top), dev)
-        pos = {r.index: k for k, r in enumerate(recs)}
-        for j, r in enumerate(top):
-            plan = PLANS.get(us[pos[r.index]].cand, ctx.numsys, None, dev)
-            timer.enqueue(j, plan, ctx.ws.sets, ctx.ws.outputs, reps=max(1, -(-refine_launches // ctx.ws.rot)))
-        lat2 = timer.read(len(top))
+            rec.timing = "screen"
+
+    def live():
+        return [k for k, r in enumerate(recs) if r.error is None and r.latency_us is not None and r.ff_ok is not False]
+
+    ok = live()
+    if ok:
+        best = min(recs[k].latency_us for k in ok)
+        sel = [k for k in ok if recs[k].latency_us <= screen_factor * best]
+        timer = Timer(len(sel), dev)
+        for j, k in enumerate(sel):
+            timer.enqueue(j, plans[k], ctx.ws.sets, ctx.ws.outputs, reps=1)
+        lat2 = timer.read(len(sel))
         timer.close()
-        for j, r in enumerate(top):
-            r.latency_us = lat2[j]
-            r.refined = True
-    for r in recs:
-        if r.latency_us is not None and not r.refined:
-            r.pruned = True  # screening measurement only (one rotation)
+        for j, k in enumerate(sel):
+            recs[k].latency_us = lat2[j]
+            recs[k].timing = "rotation"
+        top = sorted(sel, key=lambda k: (recs[k].latency_us, recs[k].index))[:refine_top]
+        timer = Timer(len(top), dev)
+        for j, k in enumerate(top):
+            timer.enqueue(j, plans[k], ctx.ws.sets, ctx.ws.outputs, reps=max(1, -(-refine_launches // rot)))
+        lat3 = timer.read(len(top))
+        timer.close()
+        for j, k in enumerate(top):
+            recs[k].latency_us = lat3[j]
+            recs[k].timing = "refined"
+            recs[k].refined = True
     return recs
 
 

@@ -24,6 +24,7 @@ def test_sweep_verdicts_and_latencies(S, w, k):
     us = us[:: max(1, len(us) // k)][:k]
     ctx = P.WorkloadContext(pop, 0)
     recs = P.evaluate_workload(ctx, us, refine_top=2, refine_launches=64)
+    assert {r.timing for r in recs} <= {"screen", "rotation", "refined"}
     assert all(r.error is None for r in recs), [r.error for r in recs if r.error]
     assert all(r.ff_ok for r in recs)
     lat = [r.latency_us for r in recs]
