@@ -120,7 +120,8 @@ typedef struct {
   int32_t no_hoist;        /* 1: do not hoist loop-invariant body nodes */
   int32_t use_tcgen05;     /* -1 off, 0 auto, 1 force where legal */
   int32_t no_tma;          /* 1: stream matmul operands with plain loads, no TMA producer warp */
-  int32_t _reserved[8];
+  int32_t trace;           /* 1: record %globaltimer at schedule events (sgm_plan_trace) */
+  int32_t _reserved[7];
 } sgm_plan_hints;
 
 typedef struct {
@@ -180,6 +181,13 @@ int sgm_plan_destroy(sgm_plan* plan);
  * reproducing the reference's NaN-initialised outputs (interp.py:147-152). */
 int sgm_plan_run(sgm_plan* plan, const void* const* inputs, void* const* outputs,
                  int init_outputs, void* stream);
+/* Timeline of the last run of a plan created with hints.trace = 1: for every
+ * launched CTA, SGM_TRACE_N (time_ns, event) pairs; entries [0, N/2) come from
+ * compute thread 0, [N/2, N) from the TMA producer lane; unused entries are 0.
+ * Events: 1 start, 2 item start, 1000+n node n, 2000+p flush at schedule position p,
+ * 5 item end; producer 3 item start, 4000+n stream of node n, 6 done. */
+#define SGM_TRACE_N 512
+int sgm_plan_trace(const sgm_plan* plan, uint64_t* host, int64_t cap_pairs, int64_t* n_pairs);
 /* Host-buffer variant: H2D of inputs, run, D2H of outputs, all on `stream`
  * (pinned staging owned by the plan).  This is the e2e path. */
 int sgm_plan_run_host(sgm_plan* plan, const void* const* host_inputs,

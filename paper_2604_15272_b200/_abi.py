@@ -38,7 +38,8 @@ class PlanHints(C.Structure):
     _fields_ = [
         ("max_cluster", C.c_int32), ("target_ctas", C.c_int32), ("threads", C.c_int32),
         ("smem_budget", C.c_int32), ("no_loop_split", C.c_int32), ("no_hoist", C.c_int32),
-        ("use_tcgen05", C.c_int32), ("no_tma", C.c_int32), ("_reserved", C.c_int32 * 8),
+        ("use_tcgen05", C.c_int32), ("no_tma", C.c_int32), ("trace", C.c_int32),
+        ("_reserved", C.c_int32 * 7),
     ]
 
 
@@ -78,6 +79,7 @@ SYMBOLS = {
     "sgm_plan_run_host": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p], C.c_int),
     "sgm_plan_time": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
                        C.c_void_p, C.POINTER(C.c_double)], C.c_int),
+    "sgm_plan_trace": ([C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "sgm_timer_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "sgm_timer_enqueue": ([C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int,
                            C.c_int, C.c_void_p], C.c_int),

@@ -96,6 +96,7 @@ struct Node {
   bool tma = false;  // B streamed by the TMA producer warp through the smem ring
   int tma_id = -1;
   int kc = 64;       // rows of B per ring stage
+  int bw = 64;       // columns of B per TMA box (fp32 path)
 };
 
 struct Class {
@@ -153,6 +154,7 @@ struct Gen {
   std::map<std::pair<int, int>, int> flush_tmp_off;  // (pos,node) -> smem offset
   int smem_peak = 0;
   i64 scratch_per_cta = 0;
+  i64 trace_off = -1;
   int budget = 200 * 1024;
   // TMA producer warp + ring (any tma matmul)
   bool prod = false;
@@ -802,11 +804,15 @@ struct Gen {
             int cols = 32;
             while (cols < ntl * 16) cols *= 2;
             x.tc_cols = cols;
-          } else if (ns == SGM_F32 && M <= 8 && K % 8 == 0 && (d3 * 4) % 16 == 0) {
+          } else if (ns == SGM_F32 && M <= 8 && K % 8 == 0 && NN % 8 == 0 && (d3 * 4) % 16 == 0) {
             x.tma = true;
             ++ntma;
             x.tc = false;
-            x.kc = K % 64 == 0 ? 64 : (K % 32 == 0 ? 32 : (K % 16 == 0 ? 16 : 8));
+            x.bw = NN >= 64 ? 64 : (NN >= 32 ? 32 : (NN >= 16 ? 16 : 8));
+            while (x.bw > 8 && NN % x.bw) x.bw /= 2;
+            i64 kmax = std::min<i64>(256, kSlot / (x.bw * 4));
+            x.kc = 8;
+            while (x.kc * 2 <= kmax && K % (x.kc * 2) == 0) x.kc *= 2;
             i64 a0 = (a.sl[0] > 1) ? x.sl[0] : 1, a1 = (a.sl[1] > 1) ? x.sl[1] : 1;
             x.at_bytes = a0 * a1 * K * M * 4;
             x.red_bytes = (i64)(NT / 32) * M * 64 * 4;
@@ -1072,6 +1078,7 @@ struct Gen {
     const Node& b = nodes[x.in[1]];
     std::string J = in_loop ? "j" : std::to_string(nloop - 1);
     i64 K = a.sl[3], NN = x.sl[3];
+    os << "      SGM_TRP(" << 4000 + n << ");\n";
     os << "      { // stream for node " << n << "\n";
     os << "        const int c0 = " << coord_expr(b, 3, J) << ", c1 = " << coord_expr(b, 2, J) << ", c2 = "
        << coord_expr(b, 1, J) << ", c3 = " << coord_expr(b, 0, J) << ";\n";
@@ -1092,12 +1099,13 @@ struct Gen {
          << "], c0 + t * 128 + 64, c1 + kc * " << x.kc << ", d2, d3, &full[slot]);\n";
       os << "            }\n";
     } else {
-      i64 nt64 = (NN + 63) / 64;
-      os << "          for (int t = 0; t < " << nt64 << "; ++t)\n";
+      i64 ntb = (NN + x.bw - 1) / x.bw;
+      os << "          for (int t = 0; t < " << ntb << "; ++t)\n";
       os << "            for (int kc = 0; kc < " << K / x.kc << "; ++kc) {\n";
       os << "              const unsigned slot = sgm::ring_acquire<" << ringS << ">(empty, pq++);\n";
-      os << "              sgm::mbar_expect_tx(&full[slot], " << x.kc * 256 << ");\n";
-      os << "              sgm::tma_load_4d(ring + slot * sgm::SLOT, &a.tm[" << x.tma_id << "], c0 + t * 64, c1 + kc * "
+      os << "              sgm::mbar_expect_tx(&full[slot], " << x.kc * x.bw * 4 << ");\n";
+      os << "              sgm::tma_load_4d(ring + slot * sgm::SLOT, &a.tm[" << x.tma_id << "], c0 + t * " << x.bw
+         << ", c1 + kc * "
          << x.kc << ", d2, d3, &full[slot]);\n";
       os << "            }\n";
     }
@@ -1108,6 +1116,7 @@ struct Gen {
     os << "    if (tid == NT) {\n      unsigned pq = 0;\n";
     os << "      for (long long item = cid; item < " << LB * FP << "LL; item += ncl) {\n";
     emit_item_vars("      ");
+    os << "      SGM_TRP(3);\n";
     bool in_loop = false;
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
@@ -1121,7 +1130,7 @@ struct Gen {
         emit_producer_node(e.node, in_loop);
       }
     }
-    os << "      }\n    }\n    return;\n";
+    os << "      }\n      SGM_TRP(6);\n    }\n    return;\n";
   }
 
   // vector width for a loader (x) or a saver (x = saver node, sl = its input's slice)
@@ -1290,8 +1299,8 @@ struct Gen {
              << ", tmem_base, ring, full, empty, done, sq, sdph);\n";
         } else if (x.tma) {
           os << "    sgm::mm_stream_f32<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
-             << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS
-             << ", NT>(" << tile_ptr(n) << ", " << pa << ", (float*)(sm + " << x.at_off << "), (float*)(sm + "
+             << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << x.bw << ", "
+             << ringS << ", NT>(" << tile_ptr(n) << ", " << pa << ", (float*)(sm + " << x.at_off << "), (float*)(sm + "
              << x.red_off << "), ring, full, empty, sq);\n";
         } else if (x.gemv && x.tc) {
           os << "    sgm::mm_gemv_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
@@ -1358,8 +1367,22 @@ struct Gen {
     }
     if (LP > 1) os << "  const int jp = (int)((crank >> " << loop_shift << ") & " << (LP - 1) << "u);\n";
     else os << "  const int jp = 0; (void)jp;\n";
+    if (d.hints.trace) {
+      trace_off = scratch_per_cta;
+      scratch_per_cta += SGM_TRACE_N * 16;
+    }
     if (scratch_per_cta > 0)
       os << "  unsigned char* scr = (unsigned char*)a.scratch + bid * " << scratch_per_cta << "LL;\n";
+    if (d.hints.trace) {
+      os << "  unsigned long long* trc = (unsigned long long*)(scr + " << trace_off << ");\n";
+      os << "  unsigned tpos = 0, ppos = " << SGM_TRACE_N / 2 << ";\n";
+      os << "#define SGM_TR(ev) do { if (tid == 0 && tpos < " << SGM_TRACE_N / 2
+         << "u) { trc[2 * tpos] = sgm::gtimer(); trc[2 * tpos + 1] = (ev); ++tpos; } } while (0)\n";
+      os << "#define SGM_TRP(ev) do { if (ppos < " << SGM_TRACE_N
+         << "u) { trc[2 * ppos] = sgm::gtimer(); trc[2 * ppos + 1] = (ev); ++ppos; } } while (0)\n";
+    } else {
+      os << "#define SGM_TR(ev) do {} while (0)\n#define SGM_TRP(ev) do {} while (0)\n";
+    }
     for (int n = 0; n < (int)nodes.size(); ++n) {
       const Node& x = nodes[n];
       if (x.store == ST_SMEM && x.kind != SGM_OUTPUT)
@@ -1400,8 +1423,10 @@ struct Gen {
       os << "  __shared__ unsigned tmem_slot;\n";
       os << "  const unsigned tmem_base = sgm::tmem_alloc<NT>(&tmem_slot, " << tmem_cols << "u);\n";
     }
+    os << "  SGM_TR(1);\n";
     os << "  for (long long item = cid; item < " << LB * FP << "LL; item += ncl) {\n";
     emit_item_vars("  ");
+    os << "  SGM_TR(2);\n";
     bool in_loop = false;
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
@@ -1416,11 +1441,14 @@ struct Gen {
         os << "  }\n";
         in_loop = false;
       } else if (e.type == Ev::FLUSH) {
+        os << "  SGM_TR(" << 2000 + p << ");\n";
         emit_flush(e.flush, p);
       } else {
+        if (nodes[e.node].kind == SGM_MATMUL || nodes[e.node].kind == SGM_SUM) os << "  SGM_TR(" << 1000 + e.node << ");\n";
         emit_node(e.node, in_loop);
       }
     }
+    os << "  SGM_TR(5);\n";
     os << "  sgm::csync<NT>();  // tiles are reused by the next item\n  }\n";
     if (tmem_cols) os << "  sgm::tmem_free<NT>(tmem_base, " << tmem_cols << "u);\n";
     os << "}\n";
@@ -1467,7 +1495,7 @@ struct Gen {
       TmaSpec t;
       t.slot = b.slot;
       t.elem_bytes = es;
-      t.box0 = 64;
+      t.box0 = x.tc ? 64 : x.bw;
       t.box1 = x.kc;
       t.swizzle128 = x.tc ? 1 : 0;
       for (int k = 0; k < 4; ++k) t.dims[k] = in_dims[b.slot][k];
@@ -1476,6 +1504,8 @@ struct Gen {
     R.smem_bytes = smem_peak;
     R.loop_parts = LP;
     R.scratch_bytes = scratch_per_cta * R.ctas;
+    R.scratch_per_cta = scratch_per_cta;
+    R.trace_off = trace_off;
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) R.n_tcgen05++;
     std::ostringstream s;

@@ -32,6 +32,8 @@ struct GenResult {
   int loop_parts = 1;
   int64_t free_parts = 1;
   int64_t scratch_bytes = 0;   // total global scratch (all CTAs)
+  int64_t scratch_per_cta = 0;
+  int64_t trace_off = -1;      // byte offset of the trace region inside each CTA's scratch
   int n_tcgen05 = 0;
   int n_tma = 0;               // streamed matmuls fed by the TMA producer warp
   int ring_slots = 0;

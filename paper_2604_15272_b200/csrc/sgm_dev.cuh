@@ -180,6 +180,11 @@ template <class N, class T> __device__ __forceinline__ typename N::C cvs(T v) {
 // ---------------------------------------------------------------------------
 // Warp / cluster primitives
 
+__device__ __forceinline__ u64 gtimer() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ u32 cluster_rank() {
   u32 r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -811,26 +816,29 @@ __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const floa
 }
 
 // Streamed fp32 contraction on CUDA cores.  Stage (t, kc) = one TMA box
-// {64 n, KC k} (no swizzle, row-major [KC][64]).  Thread layout: lane = cg + 8*kq
-// (cg: 8-column group, kq: 0..3), k-lane kl = warp*4 + kq strides the KC rows;
-// per k each thread reads 8 columns (2 x LDS.128) and A[k][0..M) (broadcast
-// within the 8 lanes of a k-lane), 8*M FMAs.  Partials reduce with shuffles over
-// kq, then across warps through `red` (NW*M*64 floats).  A thread owns columns
-// cg*4.. and 32+cg*4.. so each quarter-warp LDS.128 phase reads 128 contiguous
-// bytes (conflict-free); each warp's lane 0
-// releases the slot (empty count = NT/32).
-template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int NT>
+// {BW n, KC k} (no swizzle, row-major [KC][BW]; BW in {8,16,32,64} matches the
+// slice so nothing is over-read).  Thread layout: CGN = BW/8 column groups,
+// lane = cg + CGN*kq; k-lane kl = warp*(32/CGN) + kq strides the KC rows.  A
+// thread owns columns cg*4.. and BW/2+cg*4.. so each quarter-warp LDS.128 phase
+// reads contiguous bytes (conflict-free); per k it also reads A[k][0..M)
+// (broadcast within a k-lane) and issues 8*M FMAs.  Partials reduce with
+// shuffles over kq, then across warps through `red` (NW*M*64 floats); each
+// warp's lane 0 releases the slot (empty count = NT/32).
+template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int BW, int S, int NT>
 __device__ __forceinline__ void mm_stream_f32(float* __restrict__ out, const float* __restrict__ A,
                                               float* __restrict__ at, float* __restrict__ red, unsigned char* ring,
                                               u64* full, u64* empty, u32& q) {
-  constexpr int NT64 = (NN + 63) / 64;
+  constexpr int NTB = (NN + BW - 1) / BW;
   constexpr int NKC = K / KC;
   constexpr int NW = NT / 32;
-  constexpr int KL = NW * 4;
+  constexpr int CGN = BW / 8;
+  constexpr int KQ = 32 / CGN;
+  constexpr int KL = NW * KQ;
   constexpr int A0 = SA0 ? B0 : 1, A1 = SA1 ? B1 : 1;
-  static_assert(K % KC == 0 && KC * 256 <= SLOT && M <= 8 && NT % 32 == 0, "mm_stream_f32 shape");
+  static_assert(K % KC == 0 && KC * BW * 4 <= SLOT && M <= 8 && NT % 32 == 0 && BW >= 8 && BW <= 64 &&
+                (BW & (BW - 1)) == 0, "mm_stream_f32 shape");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cg = lane & 7, kq = lane >> 3, kl = warp * 4 + kq;
+  const int cg = lane % CGN, kq = lane / CGN, kl = warp * KQ + kq;
   // k-major copy of A: at[ab][k][m]
   for (int e = tid; e < A0 * A1 * K * M; e += NT) {
     const int m = e % M;
@@ -844,7 +852,7 @@ __device__ __forceinline__ void mm_stream_f32(float* __restrict__ out, const flo
     const int b1 = bi % B1, b0 = bi / B1;
     const float* pa = at + (i64)((SA0 ? b0 : 0) * A1 + (SA1 ? b1 : 0)) * K * M;
 #pragma unroll 1
-    for (int t = 0; t < NT64; ++t) {
+    for (int t = 0; t < NTB; ++t) {
       float acc[M][8];
 #pragma unroll
       for (int m = 0; m < M; ++m)
@@ -856,8 +864,8 @@ __device__ __forceinline__ void mm_stream_f32(float* __restrict__ out, const flo
         const float* st = reinterpret_cast<const float*>(ring + slot * SLOT);
 #pragma unroll 4
         for (int k = kl; k < KC; k += KL) {
-          const float4 w0 = *reinterpret_cast<const float4*>(st + k * 64 + cg * 4);
-          const float4 w1 = *reinterpret_cast<const float4*>(st + k * 64 + 32 + cg * 4);
+          const float4 w0 = *reinterpret_cast<const float4*>(st + k * BW + cg * 4);
+          const float4 w1 = *reinterpret_cast<const float4*>(st + k * BW + BW / 2 + cg * 4);
           const float* ak = pa + (i64)(kc * KC + k) * M;
           float av[M];
           if constexpr (M % 4 == 0) {
@@ -884,23 +892,23 @@ __device__ __forceinline__ void mm_stream_f32(float* __restrict__ out, const flo
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           float x = acc[m][v];
-          x += __shfl_xor_sync(0xffffffffu, x, 8);
-          x += __shfl_xor_sync(0xffffffffu, x, 16);
+#pragma unroll
+          for (int off = CGN; off < 32; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
           acc[m][v] = x;
         }
       if (kq == 0) {
 #pragma unroll
         for (int m = 0; m < M; ++m)
 #pragma unroll
-          for (int v = 0; v < 8; ++v) red[(warp * M + m) * 64 + (v >> 2) * 32 + cg * 4 + (v & 3)] = acc[m][v];
+          for (int v = 0; v < 8; ++v) red[(warp * M + m) * BW + (v >> 2) * (BW / 2) + cg * 4 + (v & 3)] = acc[m][v];
       }
       csync<NT>();
-      for (int e = tid; e < M * 64; e += NT) {
-        const int m = e / 64, c = e % 64;
+      for (int e = tid; e < M * BW; e += NT) {
+        const int m = e / BW, c = e % BW;
         float x = 0.0f;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) x += red[(w * M + m) * 64 + c];
-        const int n = t * 64 + c;
+        for (int w = 0; w < NW; ++w) x += red[(w * M + m) * BW + c];
+        const int n = t * BW + c;
         if (n < NN) out[((i64)bi * M + m) * NN + n] = x;
       }
       csync<NT>();

@@ -90,6 +90,8 @@ struct Driver {
   SGM_FN(cuMemFreeHost, void*)
   SGM_FN(cuMemcpyHtoDAsync, CUdeviceptr, const void*, size_t, CUstream)
   SGM_FN(cuMemcpyDtoHAsync, void*, CUdeviceptr, size_t, CUstream)
+  SGM_FN(cuMemcpyDtoH, void*, CUdeviceptr, size_t)
+  SGM_FN(cuCtxSynchronize)
   SGM_FN(cuMemsetD32Async, CUdeviceptr, unsigned, size_t, CUstream)
   SGM_FN(cuStreamSynchronize, CUstream)
   SGM_FN(cuStreamCreate, CUstream*, unsigned)
@@ -142,6 +144,8 @@ struct Driver {
     g &= sym(cuMemFreeHost, "cuMemFreeHost");
     g &= sym(cuMemcpyHtoDAsync, "cuMemcpyHtoDAsync_v2");
     g &= sym(cuMemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2");
+    g &= sym(cuMemcpyDtoH, "cuMemcpyDtoH_v2");
+    g &= sym(cuCtxSynchronize, "cuCtxSynchronize");
     g &= sym(cuMemsetD32Async, "cuMemsetD32Async");
     g &= sym(cuStreamSynchronize, "cuStreamSynchronize");
     g &= sym(cuStreamCreate, "cuStreamCreate");
@@ -508,6 +512,20 @@ int sgm_plan_source(const sgm_plan* p, char* buf, size_t cap, size_t* len) {
     memcpy(buf, p->gen.source.data(), n);
     buf[n] = 0;
   }
+  return SGM_OK;
+}
+
+int sgm_plan_trace(const sgm_plan* p, uint64_t* host, int64_t cap, int64_t* n) {
+  if (!p || !n) return set_err(SGM_ERR_INVALID, "null argument");
+  if (p->gen.trace_off < 0 || !p->scratch) return set_err(SGM_ERR_INVALID, "plan was not created with hints.trace");
+  int st = ensure_ctx();
+  if (st) return st;
+  *n = p->launch_ctas * SGM_TRACE_N;
+  if (!host || cap <= 0) return SGM_OK;
+  CU(D.cuCtxSynchronize());
+  for (int64_t c = 0; c < p->launch_ctas && (c + 1) * SGM_TRACE_N <= cap; ++c)
+    CU(D.cuMemcpyDtoH(host + c * SGM_TRACE_N * 2, p->scratch + (CUdeviceptr)(c * p->gen.scratch_per_cta + p->gen.trace_off),
+                      SGM_TRACE_N * 16));
   return SGM_OK;
 }
 

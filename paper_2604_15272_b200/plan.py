@@ -125,6 +125,7 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.no_hoist = int(h.get("no_hoist", 0))
     d.hints.use_tcgen05 = int(h.get("use_tcgen05", 0))
     d.hints.no_tma = int(h.get("no_tma", 0))
+    d.hints.trace = int(h.get("trace", 0))
     return d
 
 
@@ -197,6 +198,16 @@ class Plan:
         _abi.check(_abi.lib().sgm_plan_time(self._h, ip, op, len(input_sets), warmup, iters, C.c_void_p(s),
                                             C.byref(out)))
         return out.value
+
+    def trace(self):
+        """(launched CTAs, SGM_TRACE_N, 2) array of (time_ns, event) of the last run
+        (plans created with hints={"trace": 1})."""
+        import numpy as np
+        n = C.c_int64()
+        _abi.check(_abi.lib().sgm_plan_trace(self._h, None, 0, C.byref(n)))
+        buf = np.zeros((max(1, n.value), 2), dtype=np.uint64)
+        _abi.check(_abi.lib().sgm_plan_trace(self._h, buf.ctypes.data, n.value, C.byref(n)))
+        return buf.reshape(-1, 512, 2)
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -57,6 +57,24 @@ def test_streamed_matmul_bf16(S, M, K, N, x):
         assert S.Plan(cand, 2, None, 0).info["n_tcgen05"] == 1  # the tensor-core path was exercised
 
 
+@pytest.mark.parametrize("M,K,N,x", [(8, 4096, 4096, 128), (8, 4096, 4096, 1), (2, 512, 512, 16), (4, 1024, 256, 32),
+                                     (8, 256, 64, 8), (1, 128, 512, 4)])
+def test_streamed_matmul_f32(S, M, K, N, x):
+    """Column-split X.W in fp32: the TMA-ring CUDA-core consumer (box widths 8..64)."""
+    prog = _gemv_program(S, M, K, N)
+    N_ = S.ir.Node
+    blk = S.ir.Block(("x",), "i", (N_(0, "input", (), "X"), N_(1, "input", (), "W"), N_(2, "matmul", (0, 1)),
+                                   N_(3, "output", (2,), "O")))
+    cand = S.ir.Candidate(prog, blk, frozenset({("W", 1, "x"), ("O", 1, "x")}), {"x": x, "i": 1})
+    rng = np.random.default_rng(M * 1000 + N + 7)
+    X = _round(rng.standard_normal((M, K)), "f32")
+    W = _round(rng.standard_normal((K, N)), "f32")
+    got = S.run_concrete(cand, {"X": X, "W": W}, dtype="f32")["O"]
+    assert S.rel_err(got, X @ W) < TOL["f32"], S.rel_err(got, X @ W)
+    if (N // x) % 8 == 0:
+        assert "tma-f32" in S.Plan(cand, 1, None, 0).info["summary"]
+
+
 def _population_cases(S, w, k):
     from paper_2604_15272_b200 import population as P
     pop = P.load_population(w)
