@@ -97,6 +97,9 @@ struct Node {
   int tma_id = -1;
   int kc = 64;       // rows of B per ring stage
   int bw = 64;       // columns of B per TMA box (fp32 path)
+  bool inv = false;        // item-invariant: computed once per CTA, before the item loop
+  bool xb_shared = false;  // tcgen05 A^T buffer shared per A node (batch 1)
+  bool xb_build = true;    // this consumer (re)builds the shared A^T buffer
 };
 
 struct Class {
@@ -788,6 +791,7 @@ struct Gen {
         }
         // TMA-fed streaming (producer warp + ring): bf16 on tcgen05, fp32 on CUDA cores
         x.tma = false;
+        x.xb_shared = false;
         const i64 d3 = in_dims[b.slot][3];
         // every box starts 16-byte aligned iff the slice width along n is a multiple of 16 bytes
         // (all start terms are multiples of it); TMA faults on misaligned box starts
@@ -799,7 +803,8 @@ struct Gen {
             ++ntma;
             x.tc = true;
             x.kc = K % 64 == 0 ? 64 : (K % 32 == 0 ? 32 : 16);
-            x.at_bytes = 32 * K;
+            x.xb_shared = x.sl[0] * x.sl[1] == 1;
+            x.at_bytes = x.xb_shared ? 0 : 32 * K;
             x.red_bytes = 0;
             int cols = 32;
             while (cols < ntl * 16) cols *= 2;
@@ -827,6 +832,40 @@ struct Gen {
         prod = true;
         x.tma_id = id++;
       }
+  }
+
+  // Item-invariant nodes (persistent kernels): values that depend only on the
+  // CTA's cluster parts, not on the work item (grid coordinates / free parts),
+  // e.g. the activation tile of a column-split GEMV.  Computed once per CTA.
+  void invariants() {
+    u32 gdep = 0;
+    for (int g = 0; g < ngrid; ++g)
+      if (grid[g] > 1) gdep |= 1u << g;
+    auto free_split = [&](const Node& x) {
+      for (int k = 0; k < 4; ++k) {
+        int c = x.cls[k];
+        if (c >= 0 && cls[c].parts > 1 && !cls[c].cluster) return true;
+      }
+      return false;
+    };
+    for (auto& x : nodes) {
+      x.inv = false;
+      if (d.hints.no_hoist || LB * FP <= 1) continue;
+      if (x.body || x.pend || x.kind == SGM_OUTPUT || x.kind == SGM_ACCUM) continue;
+      if (x.store != ST_SMEM && x.store != ST_GLOBAL) continue;
+      if (free_split(x)) continue;
+      if (x.kind == SGM_INPUT) {
+        bool dep = false;
+        for (int k = 0; k < 4; ++k) dep = dep || (x.gmask[k] & gdep) || x.lsplit[k];
+        x.inv = !dep;
+      } else if (x.kind == SGM_MATMUL && (x.tma || nodes[x.in[0]].store == ST_VIEW || nodes[x.in[1]].store == ST_VIEW)) {
+        continue;
+      } else {
+        bool all = true;
+        for (int k = 0; k < x.nin; ++k) all = all && nodes[x.in[k]].inv;
+        x.inv = all;
+      }
+    }
   }
 
   // liveness-based smem allocation; returns peak bytes
@@ -857,12 +896,32 @@ struct Gen {
       int en = std::max(last[n], pos_of[n]);
       if (loop_begin_pos >= 0 && st < loop_begin_pos && en > loop_begin_pos) en = std::max(en, loop_end_pos);
       if (x.kind == SGM_ACCUM) en = std::max(en, loop_end_pos);
+      if (x.inv) { st = 0; en = S; }  // lives across all items
       Interval I;
       I.id = n;
       I.start = st;
       I.end = en;
       I.bytes = prod4(x.sl) * ec;
       iv.push_back(I);
+    }
+    // shared tcgen05 A^T buffers, one per A node: [first, last consumer], or the
+    // whole kernel when A is item-invariant (built once before the item loop)
+    std::map<int, std::vector<int>> xb_users;
+    for (int p = 0; p < S; ++p)
+      if (sched[p].type == Ev::NODE) {
+        const Node& x = nodes[sched[p].node];
+        if (x.kind == SGM_MATMUL && x.tma && x.tc && x.xb_shared) xb_users[x.in[0]].push_back(sched[p].node);
+      }
+    std::map<int, int> xb_iv;  // A node -> interval id
+    for (auto& kv : xb_users) {
+      const Node& a = nodes[kv.first];
+      Interval I;
+      I.id = -(1 + tcount++);
+      I.start = a.inv ? 0 : pos_of[kv.second.front()];
+      I.end = a.inv ? S : pos_of[kv.second.back()];
+      I.bytes = 32 * a.sl[3];
+      iv.push_back(I);
+      xb_iv[kv.first] = I.id;
     }
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].kind == SGM_MATMUL && nodes[n].red_bytes > 0) {
@@ -922,6 +981,14 @@ struct Gen {
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].kind == SGM_MATMUL && nodes[n].at_bytes > 0) nodes[n].at_off = (int)off_of[-(1 + t++)];
     for (auto& fi : flush_ids) flush_tmp_off[fi.first] = (int)off_of[fi.second];
+    for (auto& kv : xb_users) {
+      const bool pre = nodes[kv.first].inv;
+      for (size_t u = 0; u < kv.second.size(); ++u) {
+        Node& x = nodes[kv.second[u]];
+        x.at_off = (int)off_of[xb_iv[kv.first]];
+        x.xb_build = !pre && u == 0;
+      }
+    }
     // global scratch for tiles that did not fit
     scratch_per_cta = 0;
     for (auto& x : nodes)
@@ -938,6 +1005,7 @@ struct Gen {
       slices();
       schedule();
       matmul_choices();
+      invariants();
       smem_peak = allocate();
       const int tile_budget = prod ? std::min(budget, kSmemCap - (3 * kSlot + 1024)) : budget;
       if (smem_peak <= tile_budget) return true;
@@ -1295,7 +1363,7 @@ struct Gen {
         if (x.tma && x.tc) {
           os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS
-             << ", NT>(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
+             << ", NT, " << (x.xb_build ? "true" : "false") << ">(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
              << ", tmem_base, ring, full, empty, done, sq, sdph);\n";
         } else if (x.tma) {
           os << "    sgm::mm_stream_f32<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
@@ -1423,6 +1491,30 @@ struct Gen {
       os << "  __shared__ unsigned tmem_slot;\n";
       os << "  const unsigned tmem_base = sgm::tmem_alloc<NT>(&tmem_slot, " << tmem_cols << "u);\n";
     }
+    {
+      bool any = false;
+      for (int p = 0; p < (int)sched.size(); ++p)
+        if (sched[p].type == Ev::NODE && nodes[sched[p].node].inv) {
+          if (!any) os << "  // item-invariant values, once per CTA\n";
+          any = true;
+          emit_node(sched[p].node, false);
+        }
+      for (auto& x : nodes) {
+        if (!(x.kind == SGM_MATMUL && x.tma && x.tc && x.xb_shared)) continue;
+        const Node& a = nodes[x.in[0]];
+        if (!a.inv) continue;
+        bool first = true;  // one build per A node
+        for (auto& y : nodes)
+          if (&y == &x) break;
+          else if (y.kind == SGM_MATMUL && y.tma && y.tc && y.xb_shared && y.in[0] == x.in[0]) first = false;
+        if (!first) continue;
+        i64 sa[4];
+        dense_strides(a.sl, sa);
+        os << "  sgm::build_xb<" << x.sl[2] << ", " << a.sl[3] << ", " << sa[2] << "LL, " << sa[3] << "LL, NT>((u16*)(sm + "
+           << x.at_off << "), " << tile_ptr(x.in[0]) << ");\n";
+        os << "  sgm::fence_async_smem();\n  sgm::csync<NT>();\n";
+      }
+    }
     os << "  SGM_TR(1);\n";
     os << "  for (long long item = cid; item < " << LB * FP << "LL; item += ncl) {\n";
     emit_item_vars("  ");
@@ -1443,7 +1535,7 @@ struct Gen {
       } else if (e.type == Ev::FLUSH) {
         os << "  SGM_TR(" << 2000 + p << ");\n";
         emit_flush(e.flush, p);
-      } else {
+      } else if (!nodes[e.node].inv) {
         if (nodes[e.node].kind == SGM_MATMUL || nodes[e.node].kind == SGM_SUM) os << "  SGM_TR(" << 1000 + e.node << ");\n";
         emit_node(e.node, in_loop);
       }

@@ -747,7 +747,42 @@ __device__ __forceinline__ u64 umma_desc_sw128(u32 saddr, u32 lbo, u32 sbo) {
 // (N = 16, K-major, no swizzle; rows 8.. carry the bf16 residual of A when M <= 8).
 // Accumulators: TMEM columns t*16 .. t*16+15.  The MMA thread releases each slot
 // with tcgen05.commit on empty[slot] and signals `done` after the last stage.
-template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int NT>
+// A^T of one batch as the K-major no-swizzle MMA B operand (16 rows x K, bf16):
+// core matrix (k8, m) = 8 consecutive k of row m at byte (k8*16 + m)*16; rows
+// 8.. hold the bf16 residual a - bf16(a) when M <= 8 (16 mantissa bits overall).
+template <int M, int K, i64 SA2, i64 SA3, int NT>
+__device__ __forceinline__ void build_xb(u16* __restrict__ xb, const float* __restrict__ Ab) {
+  constexpr bool SPLIT = M <= 8;
+  for (int c = threadIdx.x; c < 2 * K; c += NT) {  // (k8, m) chunks of 8 elements
+    const int m = c & 15, k8 = c >> 4;
+    union { uint4 q; u16 h[8]; } u;
+    const int src = (m < M) ? m : ((SPLIT && m >= 8 && m - 8 < M) ? m - 8 : -1);
+    if (src < 0) {
+      u.q = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      float a[8];
+      if constexpr (SA3 == 1) {
+        const float4 a0 = *reinterpret_cast<const float4*>(Ab + (i64)src * SA2 + k8 * 8);
+        const float4 a1 = *reinterpret_cast<const float4*>(Ab + (i64)src * SA2 + k8 * 8 + 4);
+        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w; a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) a[kk] = Ab[(i64)src * SA2 + (i64)(k8 * 8 + kk) * SA3];
+      }
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const u16 hi = NBF16::st(a[kk]);
+        u.h[kk] = (m < M) ? hi : NBF16::st(a[kk] - NBF16::ld(hi));
+      }
+    }
+    *reinterpret_cast<uint4*>(xb + (i64)c * 8) = u.q;
+  }
+}
+
+// BUILD = false: the caller already built xbuf (shared A operand, or an
+// item-invariant one built once per CTA); requires B0 * B1 == 1.
+template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int NT,
+          bool BUILD = true>
 __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const float* __restrict__ A,
                                              unsigned char* __restrict__ xbuf, u32 tmem, unsigned char* ring, u64* full,
                                              u64* empty, u64* done, u32& q, u32& dph) {
@@ -756,24 +791,16 @@ __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const floa
   constexpr bool SPLIT = M <= 8;
   constexpr u32 IDESC = UMMA_IDESC_BF16_M128_N16;
   static_assert(K % KC == 0 && KC % 16 == 0 && KC * 256 <= SLOT && M <= 16 && NTL * 16 <= 512, "mm_stream_tc shape");
+  static_assert(BUILD || B0 * B1 == 1, "a prebuilt A^T covers one batch");
   u16* xb = reinterpret_cast<u16*>(xbuf);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int bi = 0; bi < B0 * B1; ++bi) {
     const int b1 = bi % B1, b0 = bi / B1;
-    const float* Ab = A + b0 * SA0 + b1 * SA1;
-    for (int e = tid; e < 16 * K; e += NT) {
-      const int kk = e & 7, m = (e >> 3) & 15, k = (e >> 7) * 8 + kk;
-      u16 v = 0;
-      if (m < M) {
-        v = NBF16::st(Ab[(i64)m * SA2 + (i64)k * SA3]);
-      } else if (SPLIT && m >= 8 && m - 8 < M) {
-        const float a = Ab[(i64)(m - 8) * SA2 + (i64)k * SA3];
-        v = NBF16::st(a - NBF16::ld(NBF16::st(a)));
-      }
-      xb[e] = v;
+    if constexpr (BUILD) {
+      build_xb<M, K, SA2, SA3, NT>(xb, A + b0 * SA0 + b1 * SA1);
+      fence_async_smem();
+      csync<NT>();
     }
-    fence_async_smem();
-    csync<NT>();
     const u32 q0 = q;
     q += NKC * NTL;
     if (tid == 0) {
