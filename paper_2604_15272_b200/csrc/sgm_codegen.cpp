@@ -164,7 +164,8 @@ struct Gen {
   bool no_tma_forced = false;
   int ringS = 0;
   int ring_off = 0;
-  static constexpr int kSlot = 16384;
+  static constexpr int kSlot = 32768;  // largest ring slot; plan_ring may pick 16 KB
+  int slotB = 32768;
   static constexpr int kSmemCap = 225 * 1024;  // dynamic smem incl. ring alignment slack
 
   Gen(const sgm_plan_desc& desc, int sms) : d(desc), num_sms(sms) {}
@@ -802,7 +803,7 @@ struct Gen {
             x.tma = true;
             ++ntma;
             x.tc = true;
-            x.kc = K % 64 == 0 ? 64 : (K % 32 == 0 ? 32 : 16);
+            x.kc = K % 128 == 0 ? 128 : (K % 64 == 0 ? 64 : (K % 32 == 0 ? 32 : 16));
             x.xb_shared = x.sl[0] * x.sl[1] == 1;
             x.at_bytes = x.xb_shared ? 0 : 32 * K;
             x.red_bytes = 0;
@@ -815,7 +816,7 @@ struct Gen {
             x.tc = false;
             x.bw = NN >= 64 ? 64 : (NN >= 32 ? 32 : (NN >= 16 ? 16 : 8));
             while (x.bw > 8 && NN % x.bw) x.bw /= 2;
-            i64 kmax = std::min<i64>(256, kSlot / (x.bw * 4));
+            i64 kmax = std::min<i64>(256, kSlot / (x.bw * 4));  // plan_ring halves it for 16 KB slots
             x.kc = 8;
             while (x.kc * 2 <= kmax && K % (x.kc * 2) == 0) x.kc *= 2;
             i64 a0 = (a.sl[0] > 1) ? x.sl[0] : 1, a1 = (a.sl[1] > 1) ? x.sl[1] : 1;
@@ -1054,18 +1055,28 @@ struct Gen {
 
   // ring geometry after the tile plan: as many 16 KB slots as fit (<= 12), capped so
   // that two CTAs share an SM when the grid exceeds one wave
+  // Measured on B200 (tools/bench_tma_ring.cu): TMA streaming reaches ~6.3 TB/s with
+  // 32 KB stages at one CTA per SM, or 16 KB stages at two CTAs per SM; 8 KB
+  // stages stall near 3.8 TB/s whatever the ring depth.
   void plan_ring() {
     if (!prod) { ringS = 0; return; }
     int base = (smem_peak + 1023) / 1024 * 1024;
-    int S = std::min(12, (kSmemCap - base - 1024) / kSlot);
     i64 ctas = LB * FP * CL;
-    if (ctas > num_sms) {
-      int S2 = (113 * 1024 - base - 1024) / kSlot;
-      if (S2 >= 4) S = std::min(S, S2);
+    slotB = 32768;
+    int S = std::min(6, (kSmemCap - base - 1024) / slotB);
+    if (ctas > num_sms) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM
+      int S2 = (110 * 1024 - base - 1024) / 16384;
+      if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); }
+    }
+    if (S < 3) { slotB = 16384; S = std::min(12, (kSmemCap - base - 1024) / slotB); }
+    for (auto& x : nodes) {
+      if (x.kind != SGM_MATMUL || !x.tma) continue;
+      if (x.tc) while (x.kc * 256 > slotB) x.kc /= 2;
+      else while (x.kc * x.bw * 4 > slotB) x.kc /= 2;
     }
     ringS = S;
     ring_off = base;
-    smem_peak = base + 1024 + S * kSlot;
+    smem_peak = base + 1024 + S * slotB;
   }
 
   // ------------------------------------------------------------ emission
@@ -1160,7 +1171,7 @@ struct Gen {
       os << "              const unsigned slot = sgm::ring_acquire<" << ringS << ">(empty, pq++);\n";
       os << "              const int nb = (" << NN << " - t * 128 > 64) ? 2 : 1;\n";
       os << "              sgm::mbar_expect_tx(&full[slot], nb * " << x.kc * 128 << ");\n";
-      os << "              unsigned char* dst = ring + slot * sgm::SLOT;\n";
+      os << "              unsigned char* dst = ring + slot * " << slotB << ";\n";
       os << "              sgm::tma_load_4d(dst, &a.tm[" << x.tma_id << "], c0 + t * 128, c1 + kc * " << x.kc
          << ", d2, d3, &full[slot]);\n";
       os << "              if (nb == 2) sgm::tma_load_4d(dst + " << x.kc * 128 << ", &a.tm[" << x.tma_id
@@ -1172,7 +1183,7 @@ struct Gen {
       os << "            for (int kc = 0; kc < " << K / x.kc << "; ++kc) {\n";
       os << "              const unsigned slot = sgm::ring_acquire<" << ringS << ">(empty, pq++);\n";
       os << "              sgm::mbar_expect_tx(&full[slot], " << x.kc * x.bw * 4 << ");\n";
-      os << "              sgm::tma_load_4d(ring + slot * sgm::SLOT, &a.tm[" << x.tma_id << "], c0 + t * " << x.bw
+      os << "              sgm::tma_load_4d(ring + slot * " << slotB << ", &a.tm[" << x.tma_id << "], c0 + t * " << x.bw
          << ", c1 + kc * "
          << x.kc << ", d2, d3, &full[slot]);\n";
       os << "            }\n";
@@ -1362,13 +1373,13 @@ struct Gen {
         std::string pb = b.store == ST_VIEW ? view_ptr(b) : tile_ptr(x.in[1]);
         if (x.tma && x.tc) {
           os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
-             << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS
-             << ", NT, " << (x.xb_build ? "true" : "false") << ">(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
+             << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS << ", "
+             << slotB << ", NT, " << (x.xb_build ? "true" : "false") << ">(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
              << ", tmem_base, ring, full, empty, done, sq, sdph);\n";
         } else if (x.tma) {
           os << "    sgm::mm_stream_f32<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << x.bw << ", "
-             << ringS << ", NT>(" << tile_ptr(n) << ", " << pa << ", (float*)(sm + " << x.at_off << "), (float*)(sm + "
+             << ringS << ", " << slotB << ", NT>(" << tile_ptr(n) << ", " << pa << ", (float*)(sm + " << x.at_off << "), (float*)(sm + "
              << x.red_off << "), ring, full, empty, sq);\n";
         } else if (x.gemv && x.tc) {
           os << "    sgm::mm_gemv_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "

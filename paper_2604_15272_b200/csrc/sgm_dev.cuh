@@ -697,13 +697,12 @@ __device__ __forceinline__ void mm_gemv_tc(float* __restrict__ out, const float*
 // A producer warp (one elected lane) walks the kernel's static sequence of
 // streamed boxes — every view operand of every streamed matmul, loop
 // iterations included — and issues cp.async.bulk.tensor loads into a ring of
-// S slots of SLOT bytes (full[s]: 1 arrival + tx bytes; empty[s]: consumer
+// S slots of SLOT bytes (a kernel constant, 16 or 32 KB; full[s]: 1 arrival + tx bytes; empty[s]: consumer
 // release).  It runs ahead of the compute warps across node and loop
 // boundaries, so HBM streaming overlaps the candidate's elementwise, reduction
 // and cluster-flush phases.  Producer and consumers enumerate the same stage
 // sequence, each with its own running counter.
 
-constexpr int SLOT = 16384;
 
 __device__ __forceinline__ void mbar_expect_tx(u64* b, u32 bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
@@ -781,7 +780,7 @@ __device__ __forceinline__ void build_xb(u16* __restrict__ xb, const float* __re
 
 // BUILD = false: the caller already built xbuf (shared A operand, or an
 // item-invariant one built once per CTA); requires B0 * B1 == 1.
-template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int NT,
+template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int SLOT, int NT,
           bool BUILD = true>
 __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const float* __restrict__ A,
                                              unsigned char* __restrict__ xbuf, u32 tmem, unsigned char* ring, u64* full,
@@ -851,7 +850,8 @@ __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const floa
 // (broadcast within a k-lane) and issues 8*M FMAs.  Partials reduce with
 // shuffles over kq, then across warps through `red` (NW*M*64 floats); each
 // warp's lane 0 releases the slot (empty count = NT/32).
-template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int BW, int S, int NT>
+template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int BW, int S, int SLOT,
+          int NT>
 __device__ __forceinline__ void mm_stream_f32(float* __restrict__ out, const float* __restrict__ A,
                                               float* __restrict__ at, float* __restrict__ red, unsigned char* ring,
                                               u64* full, u64* empty, u32& q) {
