@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cinttypes>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -82,6 +83,7 @@ struct Node {
   int off = 0;                 // smem offset or scratch offset
   std::vector<int> cons;
   u32 pend = 0;                // pending cluster bits (partial over these CTAs)
+  bool gpend = false;          // partial over gsplit work items (reduced at the tail)
   bool deferred = false;
   // matmul realisation
   bool gemv = false;
@@ -108,12 +110,13 @@ struct Class {
   bool twice = false;
   int parts = 1;
   bool cluster = false;  // split across the cluster (reduced) or free CTAs
+  bool gsplit = false;   // reduced class split over work items, reduced at the tail through global memory
   int bit_shift = 0;     // cluster rank bit field
-  i64 radix = 1;         // free-part mixed radix
+  i64 radix = 1;         // free-part / gsplit-part mixed radix
 };
 
 struct Ev {
-  enum { NODE, FLUSH, LOOP_BEGIN, LOOP_END } type;
+  enum { NODE, FLUSH, GFLUSH, LOOP_BEGIN, LOOP_END } type;
   int node = -1;
   std::vector<int> flush;
 };
@@ -141,6 +144,8 @@ struct Gen {
   i64 nloop = 1;
   i64 LB = 1;
   int LP = 1;            // loop parts
+  bool loop_gs = false;  // loop parts are gsplit work items (else cluster ranks)
+  i64 GP = 1;            // gsplit parts per reduction group
   int loop_shift = 0;
   int CL = 1;            // cluster size
   i64 FP = 1;            // free parts
@@ -162,6 +167,7 @@ struct Gen {
   // TMA producer warp + ring (any tma matmul)
   bool prod = false;
   bool no_tma_forced = false;
+  double est_us = 0;     // planner's time estimate
   int ringS = 0;
   int ring_off = 0;
   static constexpr int kSlot = 32768;  // largest ring slot; plan_ring may pick 16 KB
@@ -546,81 +552,176 @@ struct Gen {
       }
   }
 
-  void split_plan() {
-    int max_cluster = d.hints.max_cluster > 0 ? std::min(16, d.hints.max_cluster) : 8;
-    i64 target = d.hints.target_ctas > 0 ? d.hints.target_ctas : 2LL * num_sms;
-    i64 W = 0;
-    for (auto& x : nodes)
-      if (x.kind == SGM_INPUT) W += loader_traffic(x);
-    const i64 kMinBytesPerCta = 32 * 1024;
-    i64 max_parts = std::max<i64>(1, W / kMinBytesPerCta);
-    auto cost_of = [&](int c) -> i64 {
-      i64 cost = 0;
-      for (auto& x : nodes)
-        if (x.kind == SGM_INPUT && !has_cls(x, c)) cost += loader_traffic(x);
-      return cost;
-    };
-    auto loop_cost = [&]() -> i64 {
-      i64 cost = 0;
-      for (auto& x : nodes)
-        if (x.kind == SGM_INPUT && !loader_loop_split(x)) cost += loader_traffic(x);
-      return cost;
-    };
-    for (int iter = 0; iter < 64; ++iter) {
-      i64 tot = FP * CL;
-      if (LB * tot >= target || tot * 2 > max_parts) break;
-      int best = -1;
-      bool best_cluster = false;
-      i64 best_cost = 0, best_rem = 0;
-      for (int c = 0; c < (int)cls.size(); ++c) {
-        Class& C = cls[c];
-        if (C.twice) continue;
-        if (C.extent % (C.parts * 2)) continue;
-        bool isc = C.reduced;
-        if (isc && CL * 2 > max_cluster) continue;
-        i64 cost = cost_of(c);
-        i64 rem = C.extent / C.parts;
-        bool better = best == -1 || cost < best_cost || (cost == best_cost && !isc && best_cluster) ||
-                      (cost == best_cost && isc == best_cluster && rem > best_rem);
-        if (better) { best = c; best_cost = cost; best_cluster = isc; best_rem = rem; }
-      }
-      if (loop_split_ok && nloop % (LP * 2) == 0 && CL * 2 <= max_cluster) {
-        i64 cost = loop_cost();
-        i64 rem = nloop / LP;
-        bool better = best == -1 || cost < best_cost || (cost == best_cost && best_cluster && rem > best_rem);
-        if (better) { best = -2; best_cost = cost; best_cluster = true; best_rem = rem; }
-      }
-      if (best == -1) break;
-      if (best_cost * 4 > W && LB * tot * 2 > num_sms) break;  // >25% redundant traffic: not worth it
-      if (best == -2) { LP *= 2; CL *= 2; }
-      else {
-        cls[best].parts *= 2;
-        if (cls[best].reduced) { cls[best].cluster = true; CL *= 2; }
-        else FP *= 2;
-      }
+  // ---- split planning: greedy search on a cost model of the persistent kernel.
+  // A state assigns each axis class a power-of-two part count and a mode (free
+  // CTAs / cluster ranks / gsplit work items) and the for-loop a part count
+  // (cluster or gsplit).  Time model (calibrated on B200, tools/bench_tma_ring.cu,
+  // tools/gemv_probe.py): HBM-unique bytes at ~5.9 TB/s, redundant re-reads at L2
+  // speed, per-CTA stream rate <= ~60 GB/s, wave quantisation of work items over
+  // co-resident clusters, and fixed per-item costs for cluster flushes (~5 us)
+  // and gsplit tail reductions (~1.5 us).
+  struct PlanState {
+    std::vector<int> parts, mode;  // mode: 0 free, 1 cluster, 2 gsplit
+    int lp = 1, lmode = 1;
+  };
+
+  void apply_state(const PlanState& st) {
+    for (int c = 0; c < (int)cls.size(); ++c) {
+      cls[c].parts = st.parts[c];
+      cls[c].cluster = st.parts[c] > 1 && st.mode[c] == 1;
+      cls[c].gsplit = st.parts[c] > 1 && st.mode[c] == 2;
     }
+    LP = st.lp;
+    loop_gs = st.lp > 1 && st.lmode == 2;
     finalize_layout();
   }
 
+  static i64 resident_ctas(int cl, int sms) {
+    // co-resident CTAs at one CTA per SM under GPC placement of clusters
+    switch (cl) {
+      case 1: case 2: return sms;
+      case 4: return sms * 132 / 148;
+      case 8: return sms * 120 / 148;
+      default: return sms * 112 / 148;
+    }
+  }
+
+  double plan_cost(bool* valid) {
+    *valid = true;
+    if (GP > 1 && CL > 1) { *valid = false; return 1e30; }
+    slices();
+    schedule();
+    if (GP > 1 && !gs_tail_ok()) { *valid = false; return 1e30; }
+    // shared-memory feasibility of this split (tiles + A^T buffers + a minimal ring)
+    matmul_choices();
+    invariants();
+    const int peak = allocate();
+    const int cap = prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024)) : budget;
+    // soft penalty (10 us per KB over) so the search can walk out of infeasible splits
+    const double over = peak > cap ? (double)(peak - cap) / 1024.0 * 1e-5 : 0.0;
+    const i64 items = LB * FP * GP;
+    const i64 slots = std::max<i64>(1, resident_ctas(CL, num_sms) / CL);
+    const i64 rounds = (items + slots - 1) / slots;
+    const i64 active = std::min(items, slots) * CL;
+    u32 gdep = 0;
+    for (int g = 0; g < ngrid; ++g)
+      if (grid[g] > 1) gdep |= 1u << g;
+    double unique = 0, total = 0;
+    for (auto& x : nodes) {
+      if (x.kind != SGM_INPUT || x.cons.empty()) continue;
+      unique += (double)prod4(in_dims[x.slot]) * es;
+      double per = (double)prod4(x.sl) * es;
+      double reps = (x.body && x.loopdep) ? (double)nloop / LP : 1.0;
+      bool item_dep = x.body;
+      for (int k = 0; k < 4; ++k) {
+        item_dep = item_dep || (x.gmask[k] & gdep) || x.lsplit[k];
+        int c = x.cls[k];
+        item_dep = item_dep || (c >= 0 && cls[c].parts > 1 && !cls[c].cluster);
+      }
+      double execs = item_dep ? (double)items * CL : (double)active;
+      total += per * reps * execs;
+    }
+    double redundant = std::max(0.0, total - unique);
+    // gsplit partial tiles: written by every item, read back by the group's last one
+    double gs_bytes = 0;
+    for (auto& e : sched)
+      if (e.type == Ev::GFLUSH)
+        for (int f : e.flush) gs_bytes += 2.0 * (double)prod4(nodes[f].sl) * ec * items;
+    redundant += gs_bytes;
+    total += gs_bytes;
+    double t_mem = unique / 5.9e12 + redundant / 8e12;
+    double t_sm = (total / active) / 60e9;
+    double t_stream = std::max(t_mem, t_sm) * ((double)rounds * slots / std::max<i64>(1, items));
+    int cflush = 0, gflush = 0;
+    for (auto& e : sched) cflush += e.type == Ev::FLUSH, gflush += e.type == Ev::GFLUSH;
+    double t_item = 1.0e-6 + cflush * 5.0e-6 + gflush * 1.5e-6;
+    double loop_iters = loop_begin_pos >= 0 ? (double)nloop / LP : 0.0;
+    t_item += loop_iters * 0.6e-6;
+    return t_stream + (double)rounds * t_item + over;
+  }
+
+  void split_plan() {
+    const int max_cluster = d.hints.max_cluster > 0 ? std::min(16, d.hints.max_cluster) : 8;
+    PlanState cur;
+    cur.parts.assign(cls.size(), 1);
+    cur.mode.assign(cls.size(), 0);
+    apply_state(cur);
+    bool valid;
+    double best = plan_cost(&valid);
+    for (int iter = 0; iter < 48; ++iter) {
+      PlanState bst = cur;
+      double bcost = 1e30;
+      auto consider = [&](const PlanState& st) {
+        apply_state(st);
+        if (LB * FP * GP > (1LL << 22) || CL > max_cluster) return;
+        bool ok;
+        double c = plan_cost(&ok);
+        if (getenv("SGM_PLAN_DEBUG")) {
+          fprintf(stderr, "  plan iter %d: LB=%lld FP=%lld GP=%lld CL=%d LP=%d%s ok=%d cost=%.2fus |", iter, (long long)LB,
+                  (long long)FP, (long long)GP, CL, LP, loop_gs ? "g" : "", (int)ok, c * 1e6);
+          for (size_t k = 0; k < st.parts.size(); ++k) fprintf(stderr, " c%zu:%d/%d", k, st.parts[k], st.mode[k]);
+          fprintf(stderr, "\n");
+        }
+        if (ok && c < bcost) { bcost = c; bst = st; }
+      };
+      for (int c = 0; c < (int)cls.size(); ++c) {
+        const Class& C = cls[c];
+        if (C.twice || C.extent % (cur.parts[c] * 2)) continue;
+        std::vector<int> modes;
+        if (!C.reduced) modes = {0};
+        else if (cur.parts[c] > 1) modes = {cur.mode[c]};
+        else modes = {1, 2};
+        for (int m : modes) {
+          PlanState st = cur;
+          st.parts[c] *= 2;
+          st.mode[c] = m;
+          consider(st);
+        }
+      }
+      if (loop_split_ok && nloop % (cur.lp * 2) == 0) {
+        std::vector<int> modes = cur.lp > 1 ? std::vector<int>{cur.lmode} : std::vector<int>{1, 2};
+        for (int m : modes) {
+          PlanState st = cur;
+          st.lp *= 2;
+          st.lmode = m;
+          consider(st);
+        }
+      }
+      if (bcost >= best * 0.99) break;
+      best = bcost;
+      cur = bst;
+    }
+    apply_state(cur);
+    plan_cost(&valid);
+    est_us = best * 1e6;
+  }
+
   void finalize_layout() {
-    // cluster rank bit fields: loop first, then reduced classes
+    // cluster rank bit fields: loop first (unless gsplit), then cluster classes;
+    // free parts and gsplit parts as mixed radices
     int shift = 0;
     loop_shift = 0;
-    if (LP > 1) { loop_shift = 0; while ((1 << shift) < LP) ++shift; }
+    i64 gradix = 1;
+    if (LP > 1 && !loop_gs) { loop_shift = 0; while ((1 << shift) < LP) ++shift; }
+    if (LP > 1 && loop_gs) gradix = LP;
     i64 radix = 1;
     for (auto& C : cls) {
-      if (C.parts <= 1) continue;
+      if (C.parts <= 1) { C.cluster = C.gsplit = false; continue; }
       if (C.cluster) {
         C.bit_shift = shift;
         int b = 0;
         while ((1 << b) < C.parts) ++b;
         shift += b;
+      } else if (C.gsplit) {
+        C.radix = gradix;
+        gradix *= C.parts;
       } else {
         C.radix = radix;
         radix *= C.parts;
       }
     }
     FP = radix;
+    GP = gradix;
     CL = 1 << shift;
   }
 
@@ -629,24 +730,25 @@ struct Gen {
     if (!C.cluster || C.parts <= 1) return 0;
     return (u32)(C.parts - 1) << C.bit_shift;
   }
-  u32 loop_bits() const { return LP > 1 ? (u32)(LP - 1) << loop_shift : 0; }
+  u32 loop_bits() const { return (LP > 1 && !loop_gs) ? (u32)(LP - 1) << loop_shift : 0; }
+  bool class_gs(int c) const { return c >= 0 && cls[c].gsplit && cls[c].parts > 1; }
 
   // pending partials + schedule
   void schedule() {
-    for (auto& x : nodes) { x.pend = 0; x.deferred = false; }
+    for (auto& x : nodes) { x.pend = 0; x.gpend = false; x.deferred = false; }
     for (int n = 0; n < (int)nodes.size(); ++n) {
       Node& x = nodes[n];
       if (x.kind == SGM_MATMUL) {
         int c = nodes[x.in[0]].cls[3];
-        if (c >= 0) x.pend |= class_bits(c);
+        if (c >= 0) { x.pend |= class_bits(c); x.gpend = class_gs(c); }
       } else if (x.kind == SGM_SUM) {
         int c = nodes[x.in[0]].cls[x.axis + 4 - nodes[x.in[0]].rank];
-        if (c >= 0) x.pend |= class_bits(c);
+        if (c >= 0) { x.pend |= class_bits(c); x.gpend = class_gs(c); }
       }
     }
     for (int n = 0; n < (int)nodes.size(); ++n) {
       Node& x = nodes[n];
-      if (x.pend && x.body && !x.cons.empty()) {
+      if ((x.pend || x.gpend) && x.body && !x.cons.empty()) {
         bool all_acc = true;
         for (int c : x.cons) all_acc = all_acc && nodes[c].kind == SGM_ACCUM;
         x.deferred = all_acc;
@@ -654,6 +756,7 @@ struct Gen {
       if (x.kind == SGM_ACCUM) {
         const Node& p = nodes[x.in[0]];
         x.pend = (p.deferred ? p.pend : 0) | loop_bits();
+        x.gpend = (p.deferred && p.gpend) || (LP > 1 && loop_gs);
       }
     }
     sched.clear();
@@ -670,10 +773,23 @@ struct Gen {
         if (!nodes[p].deferred || nodes[p].kind == SGM_ACCUM) fl.push_back(p);
       if (fl.empty()) return;
       for (int p : fl) pending.erase(p);
-      Ev e;
-      e.type = Ev::FLUSH;
-      e.flush = fl;
-      sched.push_back(e);
+      std::vector<int> cf, gf;
+      for (int p : fl) {
+        if (nodes[p].pend) cf.push_back(p);
+        if (nodes[p].gpend) gf.push_back(p);
+      }
+      if (!cf.empty()) {
+        Ev e;
+        e.type = Ev::FLUSH;
+        e.flush = cf;
+        sched.push_back(e);
+      }
+      if (!gf.empty()) {
+        Ev e;
+        e.type = Ev::GFLUSH;
+        e.flush = gf;
+        sched.push_back(e);
+      }
     };
     auto push_node = [&](int n) {
       Node& x = nodes[n];
@@ -682,7 +798,7 @@ struct Gen {
       e.type = Ev::NODE;
       e.node = n;
       sched.push_back(e);
-      if (x.pend) pending.insert(n);
+      if (x.pend || x.gpend) pending.insert(n);
     };
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].hoist) push_node(n);
@@ -691,14 +807,21 @@ struct Gen {
     if (has_loop) {
       // hoisted partials must be complete before the loop re-reads them
       {
-        std::vector<int> fl;
+        std::vector<int> fl, gl;
         for (int p : pending)
-          if (!nodes[p].deferred) fl.push_back(p);
+          if (!nodes[p].deferred) (nodes[p].gpend ? gl : fl).push_back(p);
+        for (int p : fl) pending.erase(p);
+        for (int p : gl) pending.erase(p);
         if (!fl.empty()) {
-          for (int p : fl) pending.erase(p);
           Ev e;
           e.type = Ev::FLUSH;
           e.flush = fl;
+          sched.push_back(e);
+        }
+        if (!gl.empty()) {
+          Ev e;
+          e.type = Ev::GFLUSH;
+          e.flush = gl;
           sched.push_back(e);
         }
       }
@@ -719,6 +842,30 @@ struct Gen {
       if (!nodes[n].body) push_node(n);
   }
 
+  // A gsplit plan is legal iff its partials are reduced by a single GFLUSH after
+  // which only the group's last work item continues: nothing after it may depend
+  // on a gsplit part (slices of gsplit classes), stream (views), loop or flush again.
+  bool gs_tail_ok() const {
+    int g = -1;
+    for (int p = 0; p < (int)sched.size(); ++p)
+      if (sched[p].type == Ev::GFLUSH) {
+        if (g >= 0) return false;
+        g = p;
+      }
+    if (g < 0) return GP <= 1;
+    for (int p = g + 1; p < (int)sched.size(); ++p) {
+      const Ev& e = sched[p];
+      if (e.type != Ev::NODE) return false;
+      const Node& x = nodes[e.node];
+      if (x.gpend || x.pend) return false;
+      for (int k = 0; k < 4; ++k)
+        if (class_gs(x.cls[k])) return false;
+      for (int k = 0; k < x.nin; ++k)
+        if (nodes[x.in[k]].store == ST_VIEW) return false;
+    }
+    return true;
+  }
+
   // matmul realisation choices (depend on slices)
   void matmul_choices() {
     int ntma = 0;
@@ -729,6 +876,9 @@ struct Gen {
       const Node& b = nodes[x.in[1]];
       x.gemv = false;
       x.tc = false;
+      x.tma = false;
+      x.xb_shared = false;
+      x.xb_build = true;
       x.red_bytes = 0;
       x.at_bytes = 0;
       i64 M = x.sl[2], K = a.sl[3], NN = x.sl[3];
@@ -851,7 +1001,7 @@ struct Gen {
     };
     for (auto& x : nodes) {
       x.inv = false;
-      if (d.hints.no_hoist || LB * FP <= 1) continue;
+      if (d.hints.no_hoist || LB * FP * GP <= 1) continue;
       if (x.body || x.pend || x.kind == SGM_OUTPUT || x.kind == SGM_ACCUM) continue;
       if (x.store != ST_SMEM && x.store != ST_GLOBAL) continue;
       if (free_split(x)) continue;
@@ -882,7 +1032,7 @@ struct Gen {
       if (e.type == Ev::NODE) {
         const Node& x = nodes[e.node];
         for (int k = 0; k < x.nin; ++k) last[x.in[k]] = std::max(last[x.in[k]], p);
-      } else if (e.type == Ev::FLUSH) {
+      } else if (e.type == Ev::FLUSH || e.type == Ev::GFLUSH) {
         for (int f : e.flush) last[f] = std::max(last[f], p);
       }
     }
@@ -1028,15 +1178,25 @@ struct Gen {
         int c = nodes[big].cls[k];
         if (c < 0 || cls[c].twice) continue;
         if (cls[c].extent % (cls[c].parts * 2)) continue;
-        if (cls[c].reduced && CL * 2 > max_cluster) continue;
+        if (cls[c].reduced && GP == 1 && CL * 2 > max_cluster) continue;
         i64 rem = cls[c].extent / cls[c].parts;
         if (rem > bestrem) { bestrem = rem; bestc = c; }
       }
       if (bestc >= 0 && bestrem >= 2) {
-        cls[bestc].parts *= 2;
-        if (cls[bestc].reduced) cls[bestc].cluster = true;
+        Class& B = cls[bestc];
+        const bool was_c = B.cluster, was_g = B.gsplit;
+        B.parts *= 2;
+        if (B.reduced && B.parts == 2) {
+          if (GP > 1) B.gsplit = true;
+          else B.cluster = true;
+        }
         finalize_layout();
-        continue;
+        if (B.gsplit) {  // the reduction must still be a tail reduction
+          slices();
+          schedule();
+          if (!gs_tail_ok()) { B.parts /= 2; B.cluster = was_c; B.gsplit = was_g; finalize_layout(); bestc = -1; }
+        }
+        if (bestc >= 0) continue;
       }
       // spill the largest tile that never takes part in a DSMEM reduction
       int sp = -1;
@@ -1061,7 +1221,7 @@ struct Gen {
   void plan_ring() {
     if (!prod) { ringS = 0; return; }
     int base = (smem_peak + 1023) / 1024 * 1024;
-    i64 ctas = LB * FP * CL;
+    i64 ctas = LB * FP * GP * CL;
     slotB = 32768;
     int S = std::min(6, (kSmemCap - base - 1024) / slotB);
     if (ctas > num_sms) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM
@@ -1110,6 +1270,7 @@ struct Gen {
       for (int g = 0; g < ngrid; ++g)
         if (x.gmask[k] >> g & 1u) {
           w /= grid[g];
+          if (grid[g] == 1) continue;  // coordinate always 0
           dim << (any ? " + " : "") << gv[g] << " * " << w << "LL";
           any = true;
         }
@@ -1139,7 +1300,7 @@ struct Gen {
     for (int g = 0; g < ngrid; ++g)
       if (x.gmask[k] >> g & 1u) {
         w /= grid[g];
-        e << " + (int)" << gv[g] << " * " << w;
+        if (grid[g] > 1) e << " + (int)" << gv[g] << " * " << w;
       }
     if (x.lsplit[k]) {
       w /= nloop;
@@ -1192,8 +1353,10 @@ struct Gen {
   }
 
   void emit_producer() {
-    os << "    if (tid == NT) {\n      unsigned pq = 0;\n";
-    os << "      for (long long item = cid; item < " << LB * FP << "LL; item += ncl) {\n";
+    // wait for the compute warps' item-invariant prologue (its loads would queue
+    // behind a full ring of TMA traffic otherwise)
+    os << "    if (tid == NT) {\n      unsigned pq = 0;\n      sgm::mbar_wait(go, 0);\n";
+    os << "      for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl) {\n";
     emit_item_vars("      ");
     os << "      SGM_TRP(3);\n";
     bool in_loop = false;
@@ -1252,11 +1415,11 @@ struct Gen {
     p << "true";
     const Node& src = nodes[x.in[0]];
     for (int c = 0; c < (int)cls.size(); ++c) {
-      if (cls[c].parts <= 1) continue;
+      if (cls[c].parts <= 1 || cls[c].gsplit) continue;  // gsplit parts: only the group's last item gets here
       if (has_cls(src, c)) continue;
       p << " && " << part_var(c) << " == 0";
     }
-    if (LP > 1) p << " && jp == 0";
+    if (LP > 1 && !loop_gs) p << " && jp == 0";
     return p.str();
   }
 
@@ -1282,6 +1445,34 @@ struct Gen {
          << ", (const C*)(sm + " << flush_tmp_off.at({pos, f}) << "), crank);\n";
     }
     os << cl_sync();
+  }
+
+  // gsplit tail reduction: every work item of a group stores its partial tiles to
+  // the global workspace and counts itself in; the last one sums the partials in
+  // part order (bit-identical whatever the arrival order), resets the counter
+  // and runs the rest of the item; the others go on to their next item.
+  i64 gws_off = 0, gcnt_off = 0, gws_tile = 0, gws_end = 0;
+  void emit_gflush(const std::vector<int>& fl) {
+    i64 fo[SGM_MAX_NODES];
+    i64 tot = 0;
+    for (int f : fl) { fo[f] = tot; tot += prod4(nodes[f].sl); }
+    gws_tile = tot;
+    os << "    {\n      C* gw = (C*)((unsigned char*)a.scratch + " << gws_off << "LL);\n";
+    os << "      unsigned* gcnt = (unsigned*)((unsigned char*)a.scratch + " << gcnt_off << "LL);\n";
+    for (int f : fl)
+      os << "      for (int e = tid; e < " << prod4(nodes[f].sl) << "; e += NT) gw[(grp * " << GP << " + gpart) * "
+         << tot << "LL + " << fo[f] << " + e] = " << tile_ptr(f) << "[e];\n";
+    os << "      __threadfence();\n      sgm::csync<NT>();\n";
+    os << "      if (tid == 0) sgm_last = (atomicAdd(&gcnt[grp], 1u) == " << GP - 1 << "u);\n";
+    os << "      sgm::csync<NT>();\n    }\n";
+    os << "  if (sgm_last) {\n";
+    os << "    {\n      __threadfence();\n      const C* gw = (const C*)((unsigned char*)a.scratch + " << gws_off << "LL);\n";
+    for (int f : fl)
+      os << "      for (int e = tid; e < " << prod4(nodes[f].sl) << "; e += NT) { A acc = N::azero(); for (int q = 0; q < "
+         << GP << "; ++q) N::aadd(acc, __ldcg(&gw[(grp * " << GP << " + q) * " << tot << "LL + " << fo[f]
+         << " + e])); " << tile_ptr(f) << "[e] = N::fin(acc); }\n";
+    os << "      if (tid == 0) ((unsigned*)((unsigned char*)a.scratch + " << gcnt_off << "LL))[grp] = 0u;\n";
+    os << "      sgm::csync<NT>();\n    }\n";
   }
 
   void emit_node(int n, bool in_loop) {
@@ -1411,15 +1602,18 @@ struct Gen {
   void emit_item_vars(const char* ind) {
     static const char* gv[3] = {"gx", "gy", "gz"};
     os << ind << "long long rest = item;\n";
+    os << ind << "const long long gpart = rest % " << GP << "; rest /= " << GP << "; (void)gpart;\n";
+    os << ind << "const long long grp = rest; (void)grp;  // reduction group (gsplit)\n";
     os << ind << "const long long fpart = rest % " << FP << "; rest /= " << FP << "; (void)fpart;\n";
     for (int g = 0; g < ngrid; ++g)
       os << ind << "const long long " << gv[g] << " = rest % " << grid[g] << "; rest /= " << grid[g] << "; (void)"
          << gv[g] << ";\n";
     for (int c = 0; c < (int)cls.size(); ++c) {
       if (cls[c].parts <= 1 || cls[c].cluster) continue;
-      os << ind << "const int " << part_var(c) << " = (int)((fpart / " << cls[c].radix << "LL) % " << cls[c].parts
-         << "LL);\n";
+      os << ind << "const int " << part_var(c) << " = (int)((" << (cls[c].gsplit ? "gpart" : "fpart") << " / "
+         << cls[c].radix << "LL) % " << cls[c].parts << "LL);\n";
     }
+    if (LP > 1 && loop_gs) os << ind << "const int jp = (int)(gpart % " << LP << "LL);\n";
   }
 
   void emit() {
@@ -1444,13 +1638,9 @@ struct Gen {
       os << "  const int " << part_var(c) << " = (int)((crank >> " << cls[c].bit_shift << ") & " << (cls[c].parts - 1)
          << "u);\n";
     }
-    if (LP > 1) os << "  const int jp = (int)((crank >> " << loop_shift << ") & " << (LP - 1) << "u);\n";
-    else os << "  const int jp = 0; (void)jp;\n";
-    if (d.hints.trace) {
-      trace_off = scratch_per_cta;
-      scratch_per_cta += SGM_TRACE_N * 16;
-    }
-    if (scratch_per_cta > 0)
+    if (LP > 1 && !loop_gs) os << "  const int jp = (int)((crank >> " << loop_shift << ") & " << (LP - 1) << "u);\n";
+    else if (LP == 1) os << "  const int jp = 0; (void)jp;\n";
+    if (scratch_per_cta > 0 || GP > 1)
       os << "  unsigned char* scr = (unsigned char*)a.scratch + bid * " << scratch_per_cta << "LL;\n";
     if (d.hints.trace) {
       os << "  unsigned long long* trc = (unsigned long long*)(scr + " << trace_off << ");\n";
@@ -1471,10 +1661,11 @@ struct Gen {
     }
     if (prod) {
       // ring barriers; the producer warp (threads NT..NT+31) runs ahead of the compute warps
-      os << "  __shared__ __align__(8) unsigned long long sgm_bars[" << 2 * ringS + 2 << "];\n";
+      os << "  __shared__ __align__(8) unsigned long long sgm_bars[" << 2 * ringS + 3 << "];\n";
       os << "  unsigned long long* full = sgm_bars;\n  unsigned long long* empty = sgm_bars + " << ringS
          << ";\n  unsigned long long* done = sgm_bars + " << 2 * ringS << ";\n  unsigned long long* clbar = sgm_bars + "
-         << 2 * ringS + 1 << ";\n  (void)done; (void)clbar;\n";
+         << 2 * ringS + 1 << ";\n  unsigned long long* go = sgm_bars + " << 2 * ringS + 2
+         << ";\n  (void)done; (void)clbar; (void)go;\n";
       os << "  unsigned char* ring = sm + " << ring_off << ";\n";
       os << "  ring += (1024u - (sgm::smem_u32(ring) & 1023u)) & 1023u;\n";
       bool any_tc = false;
@@ -1482,7 +1673,7 @@ struct Gen {
       os << "  if (tid == 0) {\n";
       os << "    for (int q = 0; q < " << ringS << "; ++q) { sgm::mbar_init(&full[q], 1); sgm::mbar_init(&empty[q], "
          << (any_tc ? 1 : NT / 32) << "); }\n";
-      os << "    sgm::mbar_init(done, 1);\n    sgm::mbar_init(clbar, " << CL << ");\n";
+      os << "    sgm::mbar_init(done, 1);\n    sgm::mbar_init(clbar, " << CL << ");\n    sgm::mbar_init(go, 1);\n";
       os << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
       os << "  if (tid == NT) {\n";
       for (auto& x : nodes)
@@ -1526,8 +1717,11 @@ struct Gen {
         os << "  sgm::fence_async_smem();\n  sgm::csync<NT>();\n";
       }
     }
+    if (prod) os << "  if (tid == 0) sgm::mbar_arrive(go);  // the producer starts streaming now\n";
     os << "  SGM_TR(1);\n";
-    os << "  for (long long item = cid; item < " << LB * FP << "LL; item += ncl) {\n";
+    bool gs_open = false;
+    if (GP > 1) os << "  __shared__ unsigned sgm_last;\n";
+    os << "  for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl) {\n";
     emit_item_vars("  ");
     os << "  SGM_TR(2);\n";
     bool in_loop = false;
@@ -1546,11 +1740,16 @@ struct Gen {
       } else if (e.type == Ev::FLUSH) {
         os << "  SGM_TR(" << 2000 + p << ");\n";
         emit_flush(e.flush, p);
+      } else if (e.type == Ev::GFLUSH) {
+        os << "  SGM_TR(" << 2000 + p << ");\n";
+        emit_gflush(e.flush);
+        gs_open = true;
       } else if (!nodes[e.node].inv) {
         if (nodes[e.node].kind == SGM_MATMUL || nodes[e.node].kind == SGM_SUM) os << "  SGM_TR(" << 1000 + e.node << ");\n";
         emit_node(e.node, in_loop);
       }
     }
+    if (gs_open) os << "  }  // last work item of the reduction group\n";
     os << "  SGM_TR(5);\n";
     os << "  sgm::csync<NT>();  // tiles are reused by the next item\n  }\n";
     if (tmem_cols) os << "  sgm::tmem_free<NT>(tmem_base, " << tmem_cols << "u);\n";
@@ -1568,6 +1767,21 @@ struct Gen {
       ok = fit();
     }
     plan_ring();
+    if (d.hints.trace) {
+      trace_off = scratch_per_cta;
+      scratch_per_cta += SGM_TRACE_N * 16;
+    }
+    {
+      // gsplit workspace after the per-CTA scratch: partial tiles [group][part][tile], then counters
+      i64 gt = 0;
+      for (auto& e : sched)
+        if (e.type == Ev::GFLUSH)
+          for (int f : e.flush) gt += prod4(nodes[f].sl);
+      const i64 work_ctas = LB * FP * GP * CL;
+      gws_off = (work_ctas * scratch_per_cta + 255) / 256 * 256;
+      gcnt_off = gws_off + (LB * FP * GP * gt * ec + 255) / 256 * 256;
+      gws_end = GP > 1 ? gcnt_off + LB * FP * 4 : work_ctas * scratch_per_cta;
+    }
     if (!ok) {
       // still over budget after spilling everything spillable; the hard cap leaves
       // room for the templates' static smem under the 227 KB opt-in limit
@@ -1588,7 +1802,7 @@ struct Gen {
     R.logical_blocks = LB;
     R.cluster = CL;
     R.free_parts = FP;
-    R.ctas = LB * FP * CL;
+    R.ctas = LB * FP * GP * CL;
     R.threads = prod ? NT + 32 : NT;
     R.ring_slots = ringS;
     for (auto& x : nodes) {
@@ -1606,16 +1820,18 @@ struct Gen {
     }
     R.smem_bytes = smem_peak;
     R.loop_parts = LP;
-    R.scratch_bytes = scratch_per_cta * R.ctas;
+    R.scratch_bytes = gws_end;
     R.scratch_per_cta = scratch_per_cta;
     R.trace_off = trace_off;
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) R.n_tcgen05++;
     std::ostringstream s;
-    s << "LB=" << LB << " FP=" << FP << " CL=" << CL << " LP=" << LP << " ring=" << ringS << " smem=" << smem_peak
+    s << "LB=" << LB << " FP=" << FP << " GP=" << GP << " CL=" << CL << " LP=" << LP << (loop_gs ? "g" : "")
+      << " ring=" << ringS << "x" << slotB / 1024 << "K est=" << (int)est_us << "us smem=" << smem_peak
       << " scratch/cta=" << scratch_per_cta << " classes:";
     for (int c = 0; c < (int)cls.size(); ++c)
-      s << " c" << c << "(" << cls[c].extent << (cls[c].reduced ? "r" : "f") << "/" << cls[c].parts << ")";
+      s << " c" << c << "(" << cls[c].extent << (cls[c].reduced ? "r" : "f") << "/" << cls[c].parts
+        << (cls[c].parts > 1 ? (cls[c].cluster ? "c" : cls[c].gsplit ? "g" : "") : "") << ")";
     s << " mm:";
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].kind == SGM_MATMUL) s << " n" << n << (nodes[n].tma ? (nodes[n].tc ? "tma-tc" : "tma-f32") : nodes[n].gemv ? (nodes[n].tc ? "tc" : "gemv") : "gen") << (nodes[n].gemv ? "/vn" + std::to_string(nodes[n].vn) + "ks" + std::to_string(nodes[n].ks) : "");

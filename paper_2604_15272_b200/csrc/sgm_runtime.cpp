@@ -478,6 +478,10 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
   if (gr.scratch_bytes > 0) {
     r = D.cuMemAlloc(&p->scratch, (size_t)gr.scratch_bytes);
     if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuMemAlloc(scratch)"); }
+    // gsplit counters (and trace) start at zero; the kernels leave the counters at zero
+    r = D.cuMemsetD32Async(p->scratch, 0, (size_t)(gr.scratch_bytes + 3) / 4, nullptr);
+    if (r == CUDA_SUCCESS) r = D.cuCtxSynchronize();
+    if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "zero scratch"); }
   }
   *out = p;
   return SGM_OK;

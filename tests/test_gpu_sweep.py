@@ -54,3 +54,30 @@ def test_sweep_refutes_a_wrong_candidate(S):
     recs = P.evaluate_workload(ctx, [u_good, u_bad], refine_top=1, refine_launches=16)
     assert recs[0].ff_ok is True
     assert recs[1].error is not None or recs[1].ff_ok is False
+
+
+@pytest.mark.parametrize("w,mapping,params", [
+    ("G", "O.1.x,Wgate.1.x,Wup.1.x", {"x": 16, "i": 1}),
+    ("A", "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 1, "i": 1}),
+    ("Q", "Kt.1.x,O.1.x,Q.1.x,V.1.x", {"x": 8, "i": 1}),
+])
+@pytest.mark.parametrize("hints", [{"max_cluster": 1}, {}, {"max_cluster": 8, "no_tma": 1}])
+def test_split_plans_agree_exactly_in_the_field(S, w, mapping, params, hints):
+    """The same candidate under different physical plans (gsplit tail reductions
+    through global memory, cluster DSMEM reductions, plain loads) gives the
+    program's finite-field output bit-exactly, on repeated launches (the gsplit
+    counters reset themselves)."""
+    import torch
+    from paper_2604_15272_b200 import population as P
+    from paper_2604_15272_b200.ff import ff_fill_inputs, ff_run, ff_trial_seed
+    pop = P.load_population(w)
+    u = next(x for x in P.units(pop) if x.cand.mapping_list() == sorted(mapping.split(",")) and x.cand.params == params)
+    prog = u.cand.program
+    ins = ff_fill_inputs(prog, ff_trial_seed(3, 1, 0), 0)
+    exp = ff_run(S.ir.program_candidate(prog), ins, 0)
+    plan = S.Plan(u.cand, 3, hints, 0)
+    for _ in range(3):
+        outs = [torch.empty_like(e) for e in exp]
+        plan.run(ins, outs)
+        for g, e in zip(outs, exp):
+            assert torch.equal(g, e), (w, hints, plan.info["summary"])
