@@ -629,12 +629,22 @@ struct Gen {
         for (int f : e.flush) gs_bytes += 2.0 * (double)prod4(nodes[f].sl) * ec * items;
     redundant += gs_bytes;
     total += gs_bytes;
-    double t_mem = unique / 5.9e12 + redundant / 8e12;
+    // streamed operands that lose the TMA ring (misaligned / unsupported) stream at about half speed
+    double slow = 0;
+    for (auto& x : nodes)
+      if (x.kind == SGM_MATMUL && !x.tma && (ns == SGM_BF16 || ns == SGM_F32)) {
+        const Node& b = nodes[x.in[1]];
+        if (b.store == ST_VIEW) slow += (double)prod4(in_dims[b.slot]) * es;
+      }
+    double t_mem = (unique + slow) / 5.9e12 + redundant / 8e12;
     double t_sm = (total / active) / 60e9;
     double t_stream = std::max(t_mem, t_sm) * ((double)rounds * slots / std::max<i64>(1, items));
     int cflush = 0, gflush = 0;
     for (auto& e : sched) cflush += e.type == Ev::FLUSH, gflush += e.type == Ev::GFLUSH;
-    double t_item = 1.0e-6 + cflush * 5.0e-6 + gflush * 1.5e-6;
+    // fixed per-item work (activation loads, A^T builds, epilogues; measured 2-6 us) is
+    // largely hidden when two CTAs share an SM
+    const bool two = prod && peak + 3 * 16384 + 1024 <= 110 * 1024;
+    double t_item = (2.5e-6 + cflush * 5.0e-6 + gflush * 1.5e-6) * (two ? 0.4 : 1.0);
     double loop_iters = loop_begin_pos >= 0 ? (double)nloop / LP : 0.0;
     t_item += loop_iters * 0.6e-6;
     return t_stream + (double)rounds * t_item + over;
@@ -1039,6 +1049,25 @@ struct Gen {
     int tcount = 0;
     flush_tmp_off.clear();
     std::vector<std::pair<std::pair<int, int>, int>> flush_ids;
+    // in-place elementwise ops: the output reuses its first operand's tile when that
+    // operand has the same slice and dies at this node (each element is read and
+    // written by the same thread)
+    std::vector<int> rep(nodes.size());
+    for (int n = 0; n < (int)nodes.size(); ++n) rep[n] = n;
+    for (int p = 0; p < S; ++p) {
+      if (sched[p].type != Ev::NODE) continue;
+      const int n = sched[p].node;
+      const Node& x = nodes[n];
+      const bool ew = x.kind == SGM_EXP || x.kind == SGM_SILU || x.kind == SGM_SQUARE || x.kind == SGM_SQRT ||
+                      x.kind == SGM_SCALE || x.kind == SGM_DIV || x.kind == SGM_MUL || x.kind == SGM_ADD;
+      if (!ew || x.store != ST_SMEM || x.inv || d.hints.no_hoist) continue;
+      const Node& a = nodes[x.in[0]];
+      bool same = a.store == ST_SMEM && a.kind != SGM_ACCUM && a.kind != SGM_INPUT && !a.inv && last[x.in[0]] == p;
+      for (int k = 0; k < 4 && same; ++k) same = a.sl[k] == x.sl[k];
+      if (x.nin == 2 && x.in[1] != x.in[0] && rep[x.in[1]] == rep[x.in[0]]) same = false;
+      if (same) rep[n] = rep[x.in[0]];
+    }
+    std::map<int, Interval> groups;
     for (int n = 0; n < (int)nodes.size(); ++n) {
       Node& x = nodes[n];
       if (x.store != ST_SMEM || x.kind == SGM_OUTPUT) continue;
@@ -1048,13 +1077,21 @@ struct Gen {
       if (loop_begin_pos >= 0 && st < loop_begin_pos && en > loop_begin_pos) en = std::max(en, loop_end_pos);
       if (x.kind == SGM_ACCUM) en = std::max(en, loop_end_pos);
       if (x.inv) { st = 0; en = S; }  // lives across all items
-      Interval I;
-      I.id = n;
-      I.start = st;
-      I.end = en;
-      I.bytes = prod4(x.sl) * ec;
-      iv.push_back(I);
+      auto it = groups.find(rep[n]);
+      if (it == groups.end()) {
+        Interval I;
+        I.id = rep[n];
+        I.start = st;
+        I.end = en;
+        I.bytes = prod4(x.sl) * ec;
+        groups[rep[n]] = I;
+      } else {
+        it->second.start = std::min(it->second.start, st);
+        it->second.end = std::max(it->second.end, en);
+        it->second.bytes = std::max<i64>(it->second.bytes, prod4(x.sl) * ec);
+      }
     }
+    for (auto& kv : groups) iv.push_back(kv.second);
     // shared tcgen05 A^T buffers, one per A node: [first, last consumer], or the
     // whole kernel when A is item-invariant (built once before the item loop)
     std::map<int, std::vector<int>> xb_users;
@@ -1123,8 +1160,9 @@ struct Gen {
       peak = std::max(peak, off + I.bytes);
     }
     for (auto& x : nodes) x.off = 0;
-    for (auto& kv : off_of)
-      if (kv.first >= 0) nodes[kv.first].off = (int)kv.second;
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (nodes[n].store == ST_SMEM && nodes[n].kind != SGM_OUTPUT && off_of.count(rep[n]))
+        nodes[n].off = (int)off_of[rep[n]];
     int t = 0;
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].kind == SGM_MATMUL && nodes[n].red_bytes > 0) nodes[n].red_off = (int)off_of[-(1 + t++)];

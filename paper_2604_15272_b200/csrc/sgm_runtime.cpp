@@ -436,7 +436,7 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
   if (r != CUDA_SUCCESS) { delete p; return cu_check(r, "cuModuleLoadData"); }
   r = D.cuModuleGetFunction(&p->fn, p->mod, gr.kernel_name.c_str());
   if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuModuleGetFunction"); }
-  if (gr.smem_bytes > 48 * 1024) {
+  if (gr.smem_bytes > 0) {  // dynamic + static smem may cross the 48 KB default even below it
     r = D.cuFuncSetAttribute(p->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, gr.smem_bytes);
     if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuFuncSetAttribute(smem)"); }
   }
