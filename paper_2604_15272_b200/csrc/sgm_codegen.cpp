@@ -650,11 +650,15 @@ struct Gen {
     return t_stream + (double)rounds * t_item + over;
   }
 
-  void split_plan() {
+  // greedy descent from no split; `policy` restricts the mode of reduced classes
+  // and the loop (0: either, 1: cluster only, 2: gsplit only) since an early
+  // mode choice is never revisited
+  double greedy(int policy, PlanState& cur) {
     const int max_cluster = d.hints.max_cluster > 0 ? std::min(16, d.hints.max_cluster) : 8;
-    PlanState cur;
     cur.parts.assign(cls.size(), 1);
     cur.mode.assign(cls.size(), 0);
+    cur.lp = 1;
+    cur.lmode = 1;
     apply_state(cur);
     bool valid;
     double best = plan_cost(&valid);
@@ -667,20 +671,21 @@ struct Gen {
         bool ok;
         double c = plan_cost(&ok);
         if (getenv("SGM_PLAN_DEBUG")) {
-          fprintf(stderr, "  plan iter %d: LB=%lld FP=%lld GP=%lld CL=%d LP=%d%s ok=%d cost=%.2fus |", iter, (long long)LB,
-                  (long long)FP, (long long)GP, CL, LP, loop_gs ? "g" : "", (int)ok, c * 1e6);
+          fprintf(stderr, "  plan p%d iter %d: LB=%lld FP=%lld GP=%lld CL=%d LP=%d%s ok=%d cost=%.2fus |", policy, iter,
+                  (long long)LB, (long long)FP, (long long)GP, CL, LP, loop_gs ? "g" : "", (int)ok, c * 1e6);
           for (size_t k = 0; k < st.parts.size(); ++k) fprintf(stderr, " c%zu:%d/%d", k, st.parts[k], st.mode[k]);
           fprintf(stderr, "\n");
         }
         if (ok && c < bcost) { bcost = c; bst = st; }
       };
+      std::vector<int> rmodes = policy == 1 ? std::vector<int>{1} : policy == 2 ? std::vector<int>{2} : std::vector<int>{1, 2};
       for (int c = 0; c < (int)cls.size(); ++c) {
         const Class& C = cls[c];
         if (C.twice || C.extent % (cur.parts[c] * 2)) continue;
         std::vector<int> modes;
         if (!C.reduced) modes = {0};
         else if (cur.parts[c] > 1) modes = {cur.mode[c]};
-        else modes = {1, 2};
+        else modes = rmodes;
         for (int m : modes) {
           PlanState st = cur;
           st.parts[c] *= 2;
@@ -689,7 +694,7 @@ struct Gen {
         }
       }
       if (loop_split_ok && nloop % (cur.lp * 2) == 0) {
-        std::vector<int> modes = cur.lp > 1 ? std::vector<int>{cur.lmode} : std::vector<int>{1, 2};
+        std::vector<int> modes = cur.lp > 1 ? std::vector<int>{cur.lmode} : rmodes;
         for (int m : modes) {
           PlanState st = cur;
           st.lp *= 2;
@@ -701,7 +706,19 @@ struct Gen {
       best = bcost;
       cur = bst;
     }
-    apply_state(cur);
+    return best;
+  }
+
+  void split_plan() {
+    PlanState best_st;
+    double best = 1e30;
+    for (int policy : {2, 1, 0}) {
+      PlanState st;
+      double c = greedy(policy, st);
+      if (c < best * 0.98) { best = c; best_st = st; }
+    }
+    apply_state(best_st);
+    bool valid;
     plan_cost(&valid);
     est_us = best * 1e6;
   }
