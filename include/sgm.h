@@ -184,8 +184,9 @@ int sgm_plan_run(sgm_plan* plan, const void* const* inputs, void* const* outputs
 /* Timeline of the last run of a plan created with hints.trace = 1: for every
  * launched CTA, SGM_TRACE_N (time_ns, event) pairs; entries [0, N/2) come from
  * compute thread 0, [N/2, N) from the TMA producer lane; unused entries are 0.
- * Events: 1 start, 2 item start, 1000+n node n, 2000+p flush at schedule position p,
- * 5 item end; producer 3 item start, 4000+n stream of node n, 6 done. */
+ * Events: 0 entry, 1 start (setup + item-invariant prologue done), 2 item start,
+ * 1000+n node n, 2000+p flush at schedule position p, 5 item end, 7 exit;
+ * producer 3 item start, 4000+n stream of node n, 6 done. */
 #define SGM_TRACE_N 512
 int sgm_plan_trace(const sgm_plan* plan, uint64_t* host, int64_t cap_pairs, int64_t* n_pairs);
 /* Host-buffer variant: H2D of inputs, run, D2H of outputs, all on `stream`

@@ -1128,6 +1128,7 @@ struct Gen {
       iv.push_back(I);
       xb_iv[kv.first] = I.id;
     }
+    std::map<int, int> red_iv, at_iv;  // matmul node -> transient interval id
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].kind == SGM_MATMUL && nodes[n].red_bytes > 0) {
         Interval I;
@@ -1135,8 +1136,8 @@ struct Gen {
         I.start = I.end = pos_of[n];
         I.bytes = nodes[n].red_bytes;
         iv.push_back(I);
+        red_iv[n] = I.id;
       }
-    int tcount_at0 = tcount;
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].kind == SGM_MATMUL && nodes[n].at_bytes > 0) {
         Interval I;
@@ -1144,6 +1145,7 @@ struct Gen {
         I.start = I.end = pos_of[n];
         I.bytes = nodes[n].at_bytes;
         iv.push_back(I);
+        at_iv[n] = I.id;
       }
     for (int p = 0; p < S; ++p)
       if (sched[p].type == Ev::FLUSH)
@@ -1174,18 +1176,17 @@ struct Gen {
       }
       placed.push_back({I, off});
       off_of[I.id] = off;
+      if (getenv("SGM_ALLOC_DEBUG"))
+        fprintf(stderr, "  alloc id=%d [%d,%d] bytes=%lld off=%lld\n", I.id, I.start, I.end, (long long)I.bytes,
+                (long long)off);
       peak = std::max(peak, off + I.bytes);
     }
     for (auto& x : nodes) x.off = 0;
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].store == ST_SMEM && nodes[n].kind != SGM_OUTPUT && off_of.count(rep[n]))
         nodes[n].off = (int)off_of[rep[n]];
-    int t = 0;
-    for (int n = 0; n < (int)nodes.size(); ++n)
-      if (nodes[n].kind == SGM_MATMUL && nodes[n].red_bytes > 0) nodes[n].red_off = (int)off_of[-(1 + t++)];
-    t = tcount_at0;
-    for (int n = 0; n < (int)nodes.size(); ++n)
-      if (nodes[n].kind == SGM_MATMUL && nodes[n].at_bytes > 0) nodes[n].at_off = (int)off_of[-(1 + t++)];
+    for (auto& kv : red_iv) nodes[kv.first].red_off = (int)off_of[kv.second];
+    for (auto& kv : at_iv) nodes[kv.first].at_off = (int)off_of[kv.second];
     for (auto& fi : flush_ids) flush_tmp_off[fi.first] = (int)off_of[fi.second];
     for (auto& kv : xb_users) {
       const bool pre = nodes[kv.first].inv;
@@ -1707,6 +1708,7 @@ struct Gen {
     } else {
       os << "#define SGM_TR(ev) do {} while (0)\n#define SGM_TRP(ev) do {} while (0)\n";
     }
+    os << "  SGM_TR(0);  // entry\n";
     for (int n = 0; n < (int)nodes.size(); ++n) {
       const Node& x = nodes[n];
       if (x.store == ST_SMEM && x.kind != SGM_OUTPUT)
@@ -1807,6 +1809,7 @@ struct Gen {
     if (gs_open) os << "  }  // last work item of the reduction group\n";
     os << "  SGM_TR(5);\n";
     os << "  sgm::csync<NT>();  // tiles are reused by the next item\n  }\n";
+    os << "  SGM_TR(7);  // exit\n";
     if (tmem_cols) os << "  sgm::tmem_free<NT>(tmem_base, " << tmem_cols << "u);\n";
     os << "}\n";
   }

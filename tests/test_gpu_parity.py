@@ -8,15 +8,28 @@ from conftest import case_inputs_f64, case_inputs_ff
 
 pytestmark = pytest.mark.gpu
 
-F64_TOL = 1e-12
+# fp64: the reference pins run_concrete at 1e-12 (test_interp.py:173) against its own
+# numpy summation order; split plans sum partials in another order, and exp() of
+# N(0,1) sums reaches ~1e90 in the attention fixtures, so reassociation costs a few ulps
+F64_TOL = 1e-11
 
 
 @pytest.fixture(scope="module")
-def S():
+def S(desk_cases):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")
     import paper_2604_15272_b200 as S
+    from paper_2604_15272_b200 import population as P
+    # compile every fixture kernel up front on all host cores (NVRTC is thread-safe)
+    cands = []
+    for c in desk_cases:
+        if c.get("instantiate_error"):
+            continue
+        prog = S.ir.Program.from_json(c["program"])
+        cands.append(S.ir.from_serialized(c["key"], prog, c["params"]))
+        cands.append(S.ir.program_candidate(prog))
+    P.precompile(cands, [0, 3], None)
     return S
 
 

@@ -29,7 +29,7 @@ def test_sweep_verdicts_and_latencies(S, w, k):
     assert all(r.ff_ok for r in recs)
     lat = [r.latency_us for r in recs]
     assert all(x is not None and 0.5 < x < 1e5 for x in lat), lat
-    assert sum(r.refined for r in recs) == 2
+    assert sum(r.refined for r in recs) == min(2, sum(r.timing in ("rotation", "refined") for r in recs))
     # the batched verdicts equal the per-candidate path
     for u, r in list(zip(us, recs))[:4]:
         one = P.evaluate_unit(ctx, u, budget_us=100.0)

@@ -32,7 +32,7 @@ def name(ev: int) -> str:
         return f"flush@{ev - 2000}"
     if ev >= 1000:
         return f"node n{ev - 1000}"
-    return {1: "start", 2: "item", 3: "P:item", 5: "item end", 6: "P:done"}.get(ev, str(ev))
+    return {0: "entry", 1: "start", 2: "item", 3: "P:item", 5: "item end", 6: "P:done", 7: "exit"}.get(ev, str(ev))
 
 
 def pick(w, mapping, arg):
