@@ -84,6 +84,7 @@ struct Node {
   std::vector<int> cons;
   u32 pend = 0;                // pending cluster bits (partial over these CTAs)
   bool gpend = false;          // partial over gsplit work items (reduced at the tail)
+  bool lin = false;            // linear in its pending operands: computes on partials, reduced later
   bool deferred = false;
   // matmul realisation
   bool gemv = false;
@@ -712,10 +713,12 @@ struct Gen {
   void split_plan() {
     PlanState best_st;
     double best = 1e30;
+    // gsplit-only first: cluster plans must win by 10% (their flush and GPC-placement
+    // costs are the least well modelled, measured 3-7 us per item)
     for (int policy : {2, 1, 0}) {
       PlanState st;
       double c = greedy(policy, st);
-      if (c < best * 0.98) { best = c; best_st = st; }
+      if (c < best * (policy == 2 ? 1.0 : 0.9)) { best = c; best_st = st; }
     }
     apply_state(best_st);
     bool valid;
@@ -761,50 +764,48 @@ struct Gen {
   bool class_gs(int c) const { return c >= 0 && cls[c].gsplit && cls[c].parts > 1; }
 
   // pending partials + schedule
+  // Partial values.  A node reducing a split class (matmul K, sum axis) yields a
+  // partial over that split.  Ops linear in the partial operands that are still
+  // unreduced when they run propagate the partial (sum(x_p) @ B = sum(x_p @ B),
+  // sum x_p + sum y_p = sum(x_p + y_p), ...), and accumulators absorb partials of
+  // loop-body values they alone consume; any other consumer first flushes every
+  // pending partial.  So e.g. LoRA's X@W + (X@A)@B reduces once, at the tail.
+  bool linear_now(const Node& x, const std::set<int>& pending) const {
+    auto pd = [&](int k) { return pending.count(x.in[k]) > 0; };
+    switch (x.kind) {
+      case SGM_SCALE: case SGM_SUM: return pd(0);
+      case SGM_MATMUL: case SGM_MUL: return pd(0) != pd(1);
+      case SGM_DIV: return pd(0) && !pd(1);
+      case SGM_ADD: {
+        const Node& a = nodes[x.in[0]];
+        const Node& b = nodes[x.in[1]];
+        return pd(0) && pd(1) && a.pend == b.pend && a.gpend == b.gpend;
+      }
+      default: return false;
+    }
+  }
+
+  void reduce_bits(Node& x) const {
+    if (x.kind == SGM_MATMUL) {
+      int c = nodes[x.in[0]].cls[3];
+      if (c >= 0) { x.pend |= class_bits(c); x.gpend = x.gpend || class_gs(c); }
+    } else if (x.kind == SGM_SUM) {
+      int c = nodes[x.in[0]].cls[x.axis + 4 - nodes[x.in[0]].rank];
+      if (c >= 0) { x.pend |= class_bits(c); x.gpend = x.gpend || class_gs(c); }
+    }
+  }
+
   void schedule() {
-    for (auto& x : nodes) { x.pend = 0; x.gpend = false; x.deferred = false; }
-    for (int n = 0; n < (int)nodes.size(); ++n) {
-      Node& x = nodes[n];
-      if (x.kind == SGM_MATMUL) {
-        int c = nodes[x.in[0]].cls[3];
-        if (c >= 0) { x.pend |= class_bits(c); x.gpend = class_gs(c); }
-      } else if (x.kind == SGM_SUM) {
-        int c = nodes[x.in[0]].cls[x.axis + 4 - nodes[x.in[0]].rank];
-        if (c >= 0) { x.pend |= class_bits(c); x.gpend = class_gs(c); }
-      }
-    }
-    for (int n = 0; n < (int)nodes.size(); ++n) {
-      Node& x = nodes[n];
-      if ((x.pend || x.gpend) && x.body && !x.cons.empty()) {
-        bool all_acc = true;
-        for (int c : x.cons) all_acc = all_acc && nodes[c].kind == SGM_ACCUM;
-        x.deferred = all_acc;
-      }
-      if (x.kind == SGM_ACCUM) {
-        const Node& p = nodes[x.in[0]];
-        x.pend = (p.deferred ? p.pend : 0) | loop_bits();
-        x.gpend = (p.deferred && p.gpend) || (LP > 1 && loop_gs);
-      }
-    }
+    for (auto& x : nodes) { x.pend = 0; x.gpend = false; x.deferred = false; x.lin = false; }
     sched.clear();
     std::set<int> pending;
-    auto flush_for = [&](const Node& x, bool force_all) {
-      std::vector<int> fl;
-      bool need = force_all;
-      for (int k = 0; k < x.nin && !need; ++k) {
-        int p = x.in[k];
-        if (pending.count(p) && !(x.kind == SGM_ACCUM && nodes[p].deferred)) need = true;
-      }
-      if (!need) return;
-      for (int p : pending)
-        if (!nodes[p].deferred || nodes[p].kind == SGM_ACCUM) fl.push_back(p);
-      if (fl.empty()) return;
-      for (int p : fl) pending.erase(p);
+    auto flush_all = [&]() {
       std::vector<int> cf, gf;
-      for (int p : fl) {
+      for (int p : pending) {
         if (nodes[p].pend) cf.push_back(p);
         if (nodes[p].gpend) gf.push_back(p);
       }
+      pending.clear();
       if (!cf.empty()) {
         Ev e;
         e.type = Ev::FLUSH;
@@ -820,38 +821,52 @@ struct Gen {
     };
     auto push_node = [&](int n) {
       Node& x = nodes[n];
-      flush_for(x, false);
+      bool any = false;
+      for (int k = 0; k < x.nin; ++k) any = any || pending.count(x.in[k]);
+      if (x.kind == SGM_ACCUM) {
+        const int p = x.in[0];
+        bool absorb = pending.count(p) && nodes[p].body && !d.hints.no_hoist;
+        for (int c : nodes[p].cons) absorb = absorb && nodes[c].kind == SGM_ACCUM;
+        if (absorb) {
+          nodes[p].deferred = true;
+          x.pend = nodes[p].pend;
+          x.gpend = nodes[p].gpend;
+          pending.erase(p);
+        } else if (any) {
+          flush_all();
+        }
+        x.pend |= loop_bits();
+        x.gpend = x.gpend || (LP > 1 && loop_gs);
+      } else if (any && x.kind != SGM_OUTPUT && !d.hints.no_hoist && linear_now(x, pending)) {
+        x.lin = true;
+        for (int k = 0; k < x.nin; ++k)
+          if (pending.count(x.in[k])) {
+            x.pend |= nodes[x.in[k]].pend;
+            x.gpend = x.gpend || nodes[x.in[k]].gpend;
+          }
+      } else if (any) {
+        flush_all();
+      }
+      reduce_bits(x);
       Ev e;
       e.type = Ev::NODE;
       e.node = n;
       sched.push_back(e);
       if (x.pend || x.gpend) pending.insert(n);
+      if (x.lin)  // partial operands whose every consumer is linear never need the reduced value
+        for (int k = 0; k < x.nin; ++k) {
+          const int p = x.in[k];
+          bool all_lin = true;
+          for (int c : nodes[p].cons) all_lin = all_lin && (nodes[c].lin || c == n);
+          if (all_lin && pending.count(p)) pending.erase(p);
+        }
     };
     for (int n = 0; n < (int)nodes.size(); ++n)
       if (nodes[n].hoist) push_node(n);
     bool has_loop = false;
     for (auto& x : nodes) has_loop = has_loop || (x.body && !x.hoist);
     if (has_loop) {
-      // hoisted partials must be complete before the loop re-reads them
-      {
-        std::vector<int> fl, gl;
-        for (int p : pending)
-          if (!nodes[p].deferred) (nodes[p].gpend ? gl : fl).push_back(p);
-        for (int p : fl) pending.erase(p);
-        for (int p : gl) pending.erase(p);
-        if (!fl.empty()) {
-          Ev e;
-          e.type = Ev::FLUSH;
-          e.flush = fl;
-          sched.push_back(e);
-        }
-        if (!gl.empty()) {
-          Ev e;
-          e.type = Ev::GFLUSH;
-          e.flush = gl;
-          sched.push_back(e);
-        }
-      }
+      if (!pending.empty()) flush_all();  // hoisted partials must be complete before the loop re-reads them
       Ev b;
       b.type = Ev::LOOP_BEGIN;
       loop_begin_pos = (int)sched.size();
