@@ -600,10 +600,19 @@ struct Gen {
     const int cap = prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024)) : budget;
     // soft penalty (10 us per KB over) so the search can walk out of infeasible splits
     const double over = peak > cap ? (double)(peak - cap) / 1024.0 * 1e-5 : 0.0;
+    // residency: two CTAs per SM when the tiles leave room for a 3 x 16 KB ring in half an SM
+    const bool two = prod && peak + 3 * 16384 + 1024 <= 110 * 1024;
+    const int cps = two ? 2 : 1;
     const i64 items = LB * FP * GP;
-    const i64 slots = std::max<i64>(1, resident_ctas(CL, num_sms) / CL);
+    const i64 slots = std::max<i64>(1, resident_ctas(CL, num_sms) * cps / CL);
     const i64 rounds = (items + slots - 1) / slots;
     const i64 active = std::min(items, slots) * CL;
+    const double active_sms = std::max(1.0, std::min<double>(num_sms, (double)active / cps));
+    // bytes in flight per SM bound its stream rate (Little's law, ~3 us loaded latency)
+    const double inflight = prod ? (two ? cps * std::min<double>(6 * 16384, 110 * 1024 - peak - 1024)
+                                        : std::min<double>(6 * 32768, kSmemCap - peak - 1024))
+                                 : 64.0 * 1024;
+    const double bw_sm = std::min(60e9, std::max(32768.0, inflight) / 3e-6);
     u32 gdep = 0;
     for (int g = 0; g < ngrid; ++g)
       if (grid[g] > 1) gdep |= 1u << g;
@@ -638,75 +647,95 @@ struct Gen {
         if (b.store == ST_VIEW) slow += (double)prod4(in_dims[b.slot]) * es;
       }
     double t_mem = (unique + slow) / 5.9e12 + redundant / 8e12;
-    double t_sm = (total / active) / 60e9;
+    double t_sm = (total / active_sms) / bw_sm;
     double t_stream = std::max(t_mem, t_sm) * ((double)rounds * slots / std::max<i64>(1, items));
     int cflush = 0, gflush = 0;
     for (auto& e : sched) cflush += e.type == Ev::FLUSH, gflush += e.type == Ev::GFLUSH;
     // fixed per-item work (activation loads, A^T builds, epilogues; measured 2-6 us) is
     // largely hidden when two CTAs share an SM
-    const bool two = prod && peak + 3 * 16384 + 1024 <= 110 * 1024;
     double t_item = (2.5e-6 + cflush * 5.0e-6 + gflush * 1.5e-6) * (two ? 0.4 : 1.0);
     double loop_iters = loop_begin_pos >= 0 ? (double)nloop / LP : 0.0;
     t_item += loop_iters * 0.6e-6;
     return t_stream + (double)rounds * t_item + over;
   }
 
-  // greedy descent from no split; `policy` restricts the mode of reduced classes
-  // and the loop (0: either, 1: cluster only, 2: gsplit only) since an early
-  // mode choice is never revisited
-  double greedy(int policy, PlanState& cur) {
+  // Beam search from no split (width 4): each step doubles one class (in an
+  // allowed mode) or the loop; `policy` restricts the mode of reduced classes and
+  // the loop (0: either, 1: cluster only, 2: gsplit only).  A plain greedy
+  // descent gets trapped by early shared-memory-driven choices (e.g. splitting a
+  // GEMV's rows, which multiplies the weight stream).
+  double greedy(int policy, PlanState& out) {
     const int max_cluster = d.hints.max_cluster > 0 ? std::min(16, d.hints.max_cluster) : 8;
-    cur.parts.assign(cls.size(), 1);
-    cur.mode.assign(cls.size(), 0);
-    cur.lp = 1;
-    cur.lmode = 1;
-    apply_state(cur);
+    const bool dbg = getenv("SGM_PLAN_DEBUG") != nullptr;
+    PlanState root;
+    root.parts.assign(cls.size(), 1);
+    root.mode.assign(cls.size(), 0);
+    apply_state(root);
     bool valid;
-    double best = plan_cost(&valid);
-    for (int iter = 0; iter < 48; ++iter) {
-      PlanState bst = cur;
-      double bcost = 1e30;
+    double root_cost = plan_cost(&valid);
+    std::vector<std::pair<double, PlanState>> beam = {{root_cost, root}};
+    std::set<std::vector<int>> seen;
+    auto key = [&](const PlanState& st) {
+      std::vector<int> k = st.parts;
+      k.insert(k.end(), st.mode.begin(), st.mode.end());
+      k.push_back(st.lp);
+      k.push_back(st.lmode);
+      return k;
+    };
+    seen.insert(key(root));
+    double best = root_cost;
+    PlanState best_st = root;
+    const std::vector<int> rmodes =
+        policy == 1 ? std::vector<int>{1} : policy == 2 ? std::vector<int>{2} : std::vector<int>{1, 2};
+    for (int iter = 0; iter < 40; ++iter) {
+      std::vector<std::pair<double, PlanState>> next;
       auto consider = [&](const PlanState& st) {
+        if (!seen.insert(key(st)).second) return;
         apply_state(st);
         if (LB * FP * GP > (1LL << 22) || CL > max_cluster) return;
         bool ok;
         double c = plan_cost(&ok);
-        if (getenv("SGM_PLAN_DEBUG")) {
-          fprintf(stderr, "  plan p%d iter %d: LB=%lld FP=%lld GP=%lld CL=%d LP=%d%s ok=%d cost=%.2fus |", policy, iter,
+        if (dbg)
+          fprintf(stderr, "  plan p%d iter %d: LB=%lld FP=%lld GP=%lld CL=%d LP=%d%s ok=%d cost=%.2fus\n", policy, iter,
                   (long long)LB, (long long)FP, (long long)GP, CL, LP, loop_gs ? "g" : "", (int)ok, c * 1e6);
-          for (size_t k = 0; k < st.parts.size(); ++k) fprintf(stderr, " c%zu:%d/%d", k, st.parts[k], st.mode[k]);
-          fprintf(stderr, "\n");
-        }
-        if (ok && c < bcost) { bcost = c; bst = st; }
+        if (ok) next.push_back({c, st});
       };
-      std::vector<int> rmodes = policy == 1 ? std::vector<int>{1} : policy == 2 ? std::vector<int>{2} : std::vector<int>{1, 2};
-      for (int c = 0; c < (int)cls.size(); ++c) {
-        const Class& C = cls[c];
-        if (C.twice || C.extent % (cur.parts[c] * 2)) continue;
-        std::vector<int> modes;
-        if (!C.reduced) modes = {0};
-        else if (cur.parts[c] > 1) modes = {cur.mode[c]};
-        else modes = rmodes;
-        for (int m : modes) {
-          PlanState st = cur;
-          st.parts[c] *= 2;
-          st.mode[c] = m;
-          consider(st);
+      for (auto& bs : beam) {
+        const PlanState& cur = bs.second;
+        for (int c = 0; c < (int)cls.size(); ++c) {
+          const Class& C = cls[c];
+          if (C.twice || C.extent % (cur.parts[c] * 2)) continue;
+          std::vector<int> modes;
+          if (!C.reduced) modes = {0};
+          else if (cur.parts[c] > 1) modes = {cur.mode[c]};
+          else modes = rmodes;
+          for (int m : modes) {
+            PlanState st = cur;
+            st.parts[c] *= 2;
+            st.mode[c] = m;
+            consider(st);
+          }
+        }
+        if (loop_split_ok && nloop % (cur.lp * 2) == 0) {
+          std::vector<int> modes = cur.lp > 1 ? std::vector<int>{cur.lmode} : rmodes;
+          for (int m : modes) {
+            PlanState st = cur;
+            st.lp *= 2;
+            st.lmode = m;
+            consider(st);
+          }
         }
       }
-      if (loop_split_ok && nloop % (cur.lp * 2) == 0) {
-        std::vector<int> modes = cur.lp > 1 ? std::vector<int>{cur.lmode} : rmodes;
-        for (int m : modes) {
-          PlanState st = cur;
-          st.lp *= 2;
-          st.lmode = m;
-          consider(st);
-        }
-      }
-      if (bcost >= best * 0.99) break;
-      best = bcost;
-      cur = bst;
+      if (next.empty()) break;
+      std::sort(next.begin(), next.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      if (next.size() > 4) next.resize(4);
+      const bool improved = next.front().first < best * 0.99;
+      if (next.front().first < best) { best = next.front().first; best_st = next.front().second; }
+      // keep descending while any beam state is still (nearly) competitive
+      if (!improved && next.front().first > best * 1.5) break;
+      beam = next;
     }
+    out = best_st;
     return best;
   }
 
