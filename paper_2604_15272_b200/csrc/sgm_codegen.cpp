@@ -594,8 +594,8 @@ struct Gen {
     schedule();
     if (GP > 1 && !gs_tail_ok()) { *valid = false; return 1e30; }
     // shared-memory feasibility of this split (tiles + A^T buffers + a minimal ring)
-    matmul_choices();
     invariants();
+    matmul_choices();
     const int peak = allocate();
     const int cap = prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024)) : budget;
     // soft penalty (10 us per KB over) so the search can walk out of infeasible splits
@@ -1017,7 +1017,7 @@ struct Gen {
         const i64 d3 = in_dims[b.slot][3];
         // every box starts 16-byte aligned iff the slice width along n is a multiple of 16 bytes
         // (all start terms are multiples of it); TMA faults on misaligned box starts
-        const bool batch_ok = x.sl[0] * x.sl[1] <= 8 && b.sl[3] == NN && b.sl[2] == K && (NN * es) % 16 == 0;
+        const bool batch_ok = x.sl[0] * x.sl[1] <= 8 && b.sl[3] == NN && b.sl[2] == K && (NN * es) % 16 == 0 && !x.inv;
         if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 && (ns == SGM_BF16 || ns == SGM_F32)) {
           if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && (d3 * 2) % 16 == 0 &&
               ntl * 16 <= 512) {
@@ -1070,18 +1070,30 @@ struct Gen {
       }
       return false;
     };
+    // a view (HBM-resident loader) whose slice does not depend on the work item
+    auto view_inv = [&](const Node& v) {
+      if (v.kind != SGM_INPUT || v.store != ST_VIEW || v.body || free_split(v)) return false;
+      for (int k = 0; k < 4; ++k)
+        if ((v.gmask[k] & gdep) || v.lsplit[k]) return false;
+      return true;
+    };
     for (auto& x : nodes) {
       x.inv = false;
       if (d.hints.no_hoist || LB * FP * GP <= 1) continue;
-      if (x.body || x.pend || x.kind == SGM_OUTPUT || x.kind == SGM_ACCUM) continue;
+      if (x.body || x.pend || x.gpend || x.kind == SGM_OUTPUT || x.kind == SGM_ACCUM) continue;
       if (x.store != ST_SMEM && x.store != ST_GLOBAL) continue;
       if (free_split(x)) continue;
       if (x.kind == SGM_INPUT) {
         bool dep = false;
         for (int k = 0; k < 4; ++k) dep = dep || (x.gmask[k] & gdep) || x.lsplit[k];
         x.inv = !dep;
-      } else if (x.kind == SGM_MATMUL && (x.tma || nodes[x.in[0]].store == ST_VIEW || nodes[x.in[1]].store == ST_VIEW)) {
-        continue;
+      } else if (x.kind == SGM_MATMUL) {
+        // e.g. LoRA's X @ A when only the output columns are split: once per CTA,
+        // reading the (L2-resident) view directly; matmul_choices keeps it off the TMA ring
+        const Node& a = nodes[x.in[0]];
+        const Node& b = nodes[x.in[1]];
+        const bool va = a.store == ST_VIEW, vb = b.store == ST_VIEW;
+        x.inv = !(va && vb) && (va ? view_inv(a) : a.inv) && (vb ? view_inv(b) : b.inv);
       } else {
         bool all = true;
         for (int k = 0; k < x.nin; ++k) all = all && nodes[x.in[k]].inv;
@@ -1255,8 +1267,8 @@ struct Gen {
     for (int iter = 0; iter < 64; ++iter) {
       slices();
       schedule();
-      matmul_choices();
       invariants();
+      matmul_choices();
       smem_peak = allocate();
       const int tile_budget = prod ? std::min(budget, kSmemCap - (3 * kSlot + 1024)) : budget;
       if (smem_peak <= tile_budget) return true;
@@ -1562,11 +1574,14 @@ struct Gen {
     for (int f : fl)
       os << "      for (int e = tid; e < " << prod4(nodes[f].sl) << "; e += NT) gw[(grp * " << GP << " + gpart) * "
          << tot << "LL + " << fo[f] << " + e] = " << tile_ptr(f) << "[e];\n";
-    os << "      __threadfence();\n      sgm::csync<NT>();\n";
-    os << "      if (tid == 0) sgm_last = (atomicAdd(&gcnt[grp], 1u) == " << GP - 1 << "u);\n";
+    // the CTA barrier orders every thread's partial stores before thread 0's
+    // acq_rel counter update (cumulativity), so one gpu-scope RMW replaces a
+    // fence per thread; the last arrival's acquire covers all groups' partials
+    os << "      sgm::csync<NT>();\n";
+    os << "      if (tid == 0) sgm_last = (sgm::atom_add_acq_rel(&gcnt[grp], 1u) == " << GP - 1 << "u);\n";
     os << "      sgm::csync<NT>();\n    }\n";
     os << "  if (sgm_last) {\n";
-    os << "    {\n      __threadfence();\n      const C* gw = (const C*)((unsigned char*)a.scratch + " << gws_off << "LL);\n";
+    os << "    {\n      const C* gw = (const C*)((unsigned char*)a.scratch + " << gws_off << "LL);\n";
     for (int f : fl)
       os << "      for (int e = tid; e < " << prod4(nodes[f].sl) << "; e += NT) { A acc = N::azero(); for (int q = 0; q < "
          << GP << "; ++q) N::aadd(acc, __ldcg(&gw[(grp * " << GP << " + q) * " << tot << "LL + " << fo[f]

@@ -180,6 +180,11 @@ template <class N, class T> __device__ __forceinline__ typename N::C cvs(T v) {
 // ---------------------------------------------------------------------------
 // Warp / cluster primitives
 
+__device__ __forceinline__ u32 atom_add_acq_rel(u32* p, u32 v) {
+  u32 old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ u64 gtimer() {
   u64 t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
