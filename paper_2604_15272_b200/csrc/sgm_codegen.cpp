@@ -100,6 +100,8 @@ struct Node {
   int tma_id = -1;
   int kc = 64;       // rows of B per ring stage
   int bw = 64;       // columns of B per TMA box (fp32 path)
+  bool staged = false;     // loader tile fetched by the producer (TMA) into a staging buffer
+  int stage_id = -1, stage_off = 0, sbox = 0;
   bool inv = false;        // item-invariant: computed once per CTA, before the item loop
   bool xb_shared = false;  // tcgen05 A^T buffer shared per A node (batch 1)
   bool xb_build = true;    // this consumer (re)builds the shared A^T buffer
@@ -167,6 +169,8 @@ struct Gen {
   int budget = 200 * 1024;
   // TMA producer warp + ring (any tma matmul)
   bool prod = false;
+  int nstaged = 0;
+  i64 stage_total = 0;   // bytes of staging buffers (after the ring)
   bool no_tma_forced = false;
   double est_us = 0;     // planner's time estimate
   int ringS = 0;
@@ -597,11 +601,11 @@ struct Gen {
     invariants();
     matmul_choices();
     const int peak = allocate();
-    const int cap = prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024)) : budget;
+    const int cap = prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024) - (int)stage_total) : budget;
     // soft penalty (10 us per KB over) so the search can walk out of infeasible splits
     const double over = peak > cap ? (double)(peak - cap) / 1024.0 * 1e-5 : 0.0;
     // residency: two CTAs per SM when the tiles leave room for a 3 x 16 KB ring in half an SM
-    const bool two = prod && peak + 3 * 16384 + 1024 <= 110 * 1024;
+    const bool two = prod && peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
     const int cps = two ? 2 : 1;
     const i64 items = LB * FP * GP;
     const i64 slots = std::max<i64>(1, resident_ctas(CL, num_sms) * cps / CL);
@@ -609,8 +613,8 @@ struct Gen {
     const i64 active = std::min(items, slots) * CL;
     const double active_sms = std::max(1.0, std::min<double>(num_sms, (double)active / cps));
     // bytes in flight per SM bound its stream rate (Little's law, ~3 us loaded latency)
-    const double inflight = prod ? (two ? cps * std::min<double>(6 * 16384, 110 * 1024 - peak - 1024)
-                                        : std::min<double>(6 * 32768, kSmemCap - peak - 1024))
+    const double inflight = prod ? (two ? cps * std::min<double>(6 * 16384, 110 * 1024 - peak - 1024 - stage_total)
+                                        : std::min<double>(6 * 32768, kSmemCap - peak - 1024 - stage_total))
                                  : 64.0 * 1024;
     const double bw_sm = std::min(60e9, std::max(32768.0, inflight) / 3e-6);
     u32 gdep = 0;
@@ -1054,6 +1058,40 @@ struct Gen {
         prod = true;
         x.tma_id = id++;
       }
+    // per-item loader tiles of producer kernels come through TMA too, issued by the
+    // producer ahead of the item's streamed boxes (plain loads would queue behind them)
+    nstaged = 0;
+    stage_total = 0;
+    // loaders after a gsplit tail reduction run only in the group's last item: the
+    // producer cannot know which, so they keep plain loads
+    int gpos = (int)sched.size();
+    std::vector<int> npos(nodes.size(), -1);
+    for (int q = 0; q < (int)sched.size(); ++q) {
+      if (sched[q].type == Ev::GFLUSH) gpos = std::min(gpos, q);
+      if (sched[q].type == Ev::NODE) npos[sched[q].node] = q;
+    }
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& x = nodes[n];
+      x.staged = false;
+      x.stage_id = -1;
+      if (!prod || d.hints.no_tma || x.kind != SGM_INPUT || x.store != ST_SMEM || x.inv || x.body || x.cons.empty())
+        continue;
+      if (npos[n] > gpos) continue;
+      if (id >= 4) break;
+      const i64 d3 = in_dims[x.slot][3];
+      if ((x.sl[3] * es) % 16 || (d3 * es) % 16 || x.sl[0] > 256 || x.sl[1] > 256 || x.sl[2] > 256) continue;
+      i64 b3 = x.sl[3];
+      while (b3 > 256) b3 /= 2;
+      if (x.sl[3] % b3 || (b3 * es) % 16) continue;
+      const i64 bytes = prod4(x.sl) * es;
+      if (bytes > 64 * 1024) continue;
+      x.staged = true;
+      x.stage_id = nstaged++;
+      x.tma_id = id++;
+      x.sbox = (int)b3;
+      x.stage_off = (int)stage_total;
+      stage_total += (bytes + 127) / 128 * 128;
+    }
   }
 
   // Item-invariant nodes (persistent kernels): values that depend only on the
@@ -1270,7 +1308,7 @@ struct Gen {
       invariants();
       matmul_choices();
       smem_peak = allocate();
-      const int tile_budget = prod ? std::min(budget, kSmemCap - (3 * kSlot + 1024)) : budget;
+      const int tile_budget = prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024) - (int)stage_total) : budget;
       if (smem_peak <= tile_budget) return true;
       // largest smem tile
       int big = -1;
@@ -1322,7 +1360,7 @@ struct Gen {
       if (sp < 0) break;
       nodes[sp].store = ST_GLOBAL;
     }
-    return smem_peak <= (prod ? std::min(budget, kSmemCap - (3 * kSlot + 1024)) : budget);
+    return smem_peak <= (prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024) - (int)stage_total) : budget);
   }
 
   // ring geometry after the tile plan: as many 16 KB slots as fit (<= 12), capped so
@@ -1333,14 +1371,15 @@ struct Gen {
   void plan_ring() {
     if (!prod) { ringS = 0; return; }
     int base = (smem_peak + 1023) / 1024 * 1024;
+    const int stg = (int)stage_total;
     i64 ctas = LB * FP * GP * CL;
     slotB = 32768;
-    int S = std::min(6, (kSmemCap - base - 1024) / slotB);
+    int S = std::min(6, (kSmemCap - base - 1024 - stg) / slotB);
     if (ctas > num_sms) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM
-      int S2 = (110 * 1024 - base - 1024) / 16384;
+      int S2 = (110 * 1024 - base - 1024 - stg) / 16384;
       if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); }
     }
-    if (S < 3) { slotB = 16384; S = std::min(12, (kSmemCap - base - 1024) / slotB); }
+    if (S < 3) { slotB = 16384; S = std::min(12, (kSmemCap - base - 1024 - stg) / slotB); }
     for (auto& x : nodes) {
       if (x.kind != SGM_MATMUL || !x.tma) continue;
       if (x.tc) while (x.kc * 256 > slotB) x.kc /= 2;
@@ -1348,7 +1387,7 @@ struct Gen {
     }
     ringS = S;
     ring_off = base;
-    smem_peak = base + 1024 + S * slotB;
+    smem_peak = base + 1024 + S * slotB + stg;
   }
 
   // ------------------------------------------------------------ emission
@@ -1468,9 +1507,22 @@ struct Gen {
     // wait for the compute warps' item-invariant prologue (its loads would queue
     // behind a full ring of TMA traffic otherwise)
     os << "    if (tid == NT) {\n      unsigned pq = 0;\n      sgm::mbar_wait(go, 0);\n";
-    os << "      for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl) {\n";
+    os << "      unsigned pit = 0;\n";
+    os << "      for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl, ++pit) {\n";
     emit_item_vars("      ");
     os << "      SGM_TRP(3);\n";
+    for (auto& x : nodes) {
+      if (!x.staged) continue;
+      const std::string J = std::to_string(nloop - 1);
+      os << "      { // staged loader tile\n";
+      os << "        if (pit > 0u) sgm::mbar_wait(&sempty[" << x.stage_id << "], (pit - 1u) & 1u);\n";
+      os << "        sgm::mbar_expect_tx(&sfull[" << x.stage_id << "], " << prod4(x.sl) * es << "u);\n";
+      os << "        const int c0 = " << coord_expr(x, 3, J) << ", c1 = " << coord_expr(x, 2, J) << ", c2 = "
+         << coord_expr(x, 1, J) << ", c3 = " << coord_expr(x, 0, J) << ";\n";
+      os << "        for (int b = 0; b < " << x.sl[3] / x.sbox << "; ++b) sgm::tma_load_4d(stg + " << x.stage_off << " + b * "
+         << (i64)x.sbox * x.sl[0] * x.sl[1] * x.sl[2] * es << ", &a.tm[" << x.tma_id << "], c0 + b * " << x.sbox
+         << ", c1, c2, c3, &sfull[" << x.stage_id << "]);\n      }\n";
+    }
     bool in_loop = false;
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
@@ -1598,6 +1650,13 @@ struct Gen {
     switch (x.kind) {
       case SGM_INPUT: {
         if (x.store == ST_VIEW) return;  // streamed by its consumer (pointer built there)
+        if (x.staged) {
+          os << "    sgm::mbar_wait(&sfull[" << x.stage_id << "], cit & 1u);\n";
+          os << "    sgm::stage_convert<N, " << x.sl[0] << ", " << x.sl[1] << ", " << x.sl[2] << ", " << x.sl[3] << ", "
+             << x.sbox << ", NT>(" << tile_ptr(n) << ", (const S*)(stg + " << x.stage_off << "));\n";
+          os << "    sgm::csync<NT>();\n    if (tid == 0) sgm::mbar_arrive(&sempty[" << x.stage_id << "]);\n";
+          return;
+        }
         std::string off = offset_expr(x, true, J);
         const i64* st = in_strides[x.slot];
         os << "    sgm::load_tile<N, " << x.sl[0] << ", " << x.sl[1] << ", " << x.sl[2] << ", " << x.sl[3] << ", "
@@ -1777,23 +1836,27 @@ struct Gen {
     }
     if (prod) {
       // ring barriers; the producer warp (threads NT..NT+31) runs ahead of the compute warps
-      os << "  __shared__ __align__(8) unsigned long long sgm_bars[" << 2 * ringS + 3 << "];\n";
+      os << "  __shared__ __align__(8) unsigned long long sgm_bars[" << 2 * ringS + 3 + 2 * std::max(nstaged, 1) << "];\n";
       os << "  unsigned long long* full = sgm_bars;\n  unsigned long long* empty = sgm_bars + " << ringS
          << ";\n  unsigned long long* done = sgm_bars + " << 2 * ringS << ";\n  unsigned long long* clbar = sgm_bars + "
          << 2 * ringS + 1 << ";\n  unsigned long long* go = sgm_bars + " << 2 * ringS + 2
-         << ";\n  (void)done; (void)clbar; (void)go;\n";
+         << ";\n  unsigned long long* sfull = sgm_bars + " << 2 * ringS + 3 << ";\n  unsigned long long* sempty = sfull + "
+         << std::max(nstaged, 1) << ";\n  (void)done; (void)clbar; (void)go; (void)sfull; (void)sempty;\n";
+
       os << "  unsigned char* ring = sm + " << ring_off << ";\n";
       os << "  ring += (1024u - (sgm::smem_u32(ring) & 1023u)) & 1023u;\n";
+      os << "  unsigned char* stg = ring + " << ringS * slotB << "; (void)stg;  // staged loader tiles\n";
       bool any_tc = false;
       for (auto& x : nodes) any_tc = any_tc || (x.kind == SGM_MATMUL && x.tma && x.tc);
       os << "  if (tid == 0) {\n";
       os << "    for (int q = 0; q < " << ringS << "; ++q) { sgm::mbar_init(&full[q], 1); sgm::mbar_init(&empty[q], "
          << (any_tc ? 1 : NT / 32) << "); }\n";
       os << "    sgm::mbar_init(done, 1);\n    sgm::mbar_init(clbar, " << CL << ");\n    sgm::mbar_init(go, 1);\n";
+      if (nstaged) os << "    for (int q = 0; q < " << nstaged << "; ++q) { sgm::mbar_init(&sfull[q], 1); sgm::mbar_init(&sempty[q], 1); }\n";
       os << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n";
       os << "  if (tid == NT) {\n";
       for (auto& x : nodes)
-        if (x.kind == SGM_MATMUL && x.tma) os << "    sgm::tma_prefetch_desc(&a.tm[" << x.tma_id << "]);\n";
+        if ((x.kind == SGM_MATMUL && x.tma) || x.staged) os << "    sgm::tma_prefetch_desc(&a.tm[" << x.tma_id << "]);\n";
       os << "  }\n";
       os << "  __syncthreads();\n";
       if (CL > 1) os << "  sgm::cluster_sync();\n";
@@ -1837,7 +1900,8 @@ struct Gen {
     os << "  SGM_TR(1);\n";
     bool gs_open = false;
     if (GP > 1) os << "  __shared__ unsigned sgm_last;\n";
-    os << "  for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl) {\n";
+    os << "  unsigned cit = 0; (void)cit;\n";
+    os << "  for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl, ++cit) {\n";
     emit_item_vars("  ");
     os << "  SGM_TR(2);\n";
     bool in_loop = false;
@@ -1922,6 +1986,22 @@ struct Gen {
     R.ctas = LB * FP * GP * CL;
     R.threads = prod ? NT + 32 : NT;
     R.ring_slots = ringS;
+    std::vector<TmaSpec> specs(4);
+    int nspec = 0;
+    for (auto& x : nodes) {
+      if (!x.staged) continue;
+      TmaSpec t;
+      t.slot = x.slot;
+      t.elem_bytes = es;
+      t.box0 = x.sbox;
+      t.box1 = (int)x.sl[2];
+      t.box2 = (int)x.sl[1];
+      t.box3 = (int)x.sl[0];
+      t.swizzle128 = 0;
+      for (int k = 0; k < 4; ++k) t.dims[k] = in_dims[x.slot][k];
+      specs[x.tma_id] = t;
+      nspec = std::max(nspec, x.tma_id + 1);
+    }
     for (auto& x : nodes) {
       if (x.kind != SGM_MATMUL || !x.tma) continue;
       R.n_tma++;
@@ -1933,8 +2013,11 @@ struct Gen {
       t.box1 = x.kc;
       t.swizzle128 = x.tc ? 1 : 0;
       for (int k = 0; k < 4; ++k) t.dims[k] = in_dims[b.slot][k];
-      R.tmaps.push_back(t);
+      specs[x.tma_id] = t;
+      nspec = std::max(nspec, x.tma_id + 1);
     }
+    specs.resize(nspec);
+    R.tmaps = specs;
     R.smem_bytes = smem_peak;
     R.loop_parts = LP;
     R.scratch_bytes = gws_end;

@@ -14,7 +14,7 @@ namespace sgmcg {
 struct TmaSpec {
   int slot = 0;
   int elem_bytes = 2;   // 2: bf16, 4: fp32
-  int box0 = 64, box1 = 64;
+  int box0 = 64, box1 = 64, box2 = 1, box3 = 1;
   int swizzle128 = 0;
   int64_t dims[4] = {1, 1, 1, 1};
 };

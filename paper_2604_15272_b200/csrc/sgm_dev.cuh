@@ -948,6 +948,18 @@ __device__ __forceinline__ void mm_stream_f32(float* __restrict__ out, const flo
   }
 }
 
+// Staged loader tile: the producer TMA-loads the item's tile (storage type) into
+// a staging buffer laid out [D3/B3][D0][D1][D2][B3] (one box per B3 columns);
+// compute threads convert it into the dense compute-type tile.
+template <class N, int D0, int D1, int D2, int D3, int B3, int NT>
+__device__ __forceinline__ void stage_convert(typename N::C* __restrict__ dst, const typename N::S* __restrict__ stage) {
+  constexpr int ROWS = D0 * D1 * D2;
+  for (int e = threadIdx.x; e < ROWS * D3; e += NT) {
+    const int i3 = e % D3, r = e / D3;
+    dst[e] = N::ld(stage[((i64)(i3 / B3) * ROWS + r) * B3 + (i3 % B3)]);
+  }
+}
+
 // Cluster barrier among compute threads only (the producer warp may be blocked
 // on its ring and must not be counted): thread 0 of every CTA arrives on every
 // peer's `bar` (count CL) with release.cluster and waits with acquire.cluster.

@@ -268,8 +268,9 @@ int compile_cubin(const std::string& src, std::string& cubin, double& ms, int& h
   const char* hnames[2] = {"sgm_dev.cuh", "sgm_util.cuh"};
   if (nvrtcCreateProgram(&prog, src.c_str(), "sgm_kernel.cu", 2, hdrs, hnames) != NVRTC_SUCCESS)
     return set_err(SGM_ERR_NVRTC, "nvrtcCreateProgram failed");
-  const char* opts[] = {kArch, "-std=c++17", "-lineinfo", "-DNDEBUG", "--extra-device-vectorization"};
-  nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+  const char* opts[] = {kArch, "-std=c++17", "-lineinfo", "-DNDEBUG", "--extra-device-vectorization",
+                        "-diag-suppress=177,550"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 6, opts);
   if (r != NVRTC_SUCCESS) {
     size_t ls = 0;
     nvrtcGetProgramLogSize(prog, &ls);
@@ -569,7 +570,7 @@ static int encode_tmap(sgm_plan* p, int i, const void* ptr) {
   cuuint64_t gdim[4] = {(cuuint64_t)t.dims[3], (cuuint64_t)t.dims[2], (cuuint64_t)t.dims[1], (cuuint64_t)t.dims[0]};
   cuuint64_t es = (cuuint64_t)t.elem_bytes;
   cuuint64_t gstride[3] = {gdim[0] * es, gdim[0] * gdim[1] * es, gdim[0] * gdim[1] * gdim[2] * es};
-  cuuint32_t box[4] = {(cuuint32_t)t.box0, (cuuint32_t)t.box1, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)t.box0, (cuuint32_t)t.box1, (cuuint32_t)t.box2, (cuuint32_t)t.box3};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = D.cuTensorMapEncodeTiled(&p->tmaps[i],
                                         t.elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
