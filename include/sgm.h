@@ -201,14 +201,14 @@ int sgm_plan_time(sgm_plan* plan, const void* const* inputs, void* const* output
 
 /* Batched, sync-free profiling of many plans (the candidate sweep).  Slot k
  * times `reps` launches of a CUDA graph holding `rot` back-to-back launches (one
- * per rotating input set; `inputs` = rot*n_inputs pointers), after one untimed
- * warm-up launch of that graph, between two events recorded on `stream`.
+ * per rotating input set; `inputs` = rot*n_inputs pointers), after `warmup`
+ * untimed launches of that graph, between two events recorded on `stream`.
  * Nothing synchronises until sgm_timer_read, which waits for the last event and
  * returns the mean microseconds per kernel launch of slots 0..n-1. */
 typedef struct sgm_timer sgm_timer;
 int sgm_timer_create(int capacity, sgm_timer** out);
 int sgm_timer_enqueue(sgm_timer* t, int slot, sgm_plan* plan, const void* const* inputs, void* const* outputs,
-                      int rot, int reps, void* stream);
+                      int rot, int warmup, int reps, void* stream);
 int sgm_timer_read(sgm_timer* t, int n, double* us_per_launch);
 int sgm_timer_destroy(sgm_timer* t);
 

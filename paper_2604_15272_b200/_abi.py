@@ -82,7 +82,7 @@ SYMBOLS = {
     "sgm_plan_trace": ([C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "sgm_timer_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "sgm_timer_enqueue": ([C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int,
-                           C.c_int, C.c_void_p], C.c_int),
+                           C.c_int, C.c_int, C.c_void_p], C.c_int),
     "sgm_timer_read": ([C.c_void_p, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "sgm_timer_destroy": ([C.c_void_p], C.c_int),
     "sgm_compare_u32_acc": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p], C.c_int),

@@ -437,6 +437,9 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
   if (r != CUDA_SUCCESS) { delete p; return cu_check(r, "cuModuleLoadData"); }
   r = D.cuModuleGetFunction(&p->fn, p->mod, gr.kernel_name.c_str());
   if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuModuleGetFunction"); }
+  // prefer the largest shared-memory carveout: the planner counts on two CTAs per SM
+  // at ~110 KB each, which the default carveout does not always grant
+  D.cuFuncSetAttribute(p->fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
   if (gr.smem_bytes > 0) {  // dynamic + static smem may cross the 48 KB default even below it
     r = D.cuFuncSetAttribute(p->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, gr.smem_bytes);
     if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuFuncSetAttribute(smem)"); }
@@ -740,7 +743,7 @@ int sgm_timer_create(int capacity, sgm_timer** out) {
 }
 
 int sgm_timer_enqueue(sgm_timer* t, int slot, sgm_plan* p, const void* const* inputs, void* const* outputs, int rot,
-                      int reps, void* stream) {
+                      int warmup, int reps, void* stream) {
   if (!t || !p || !p->fn || slot < 0 || slot >= t->cap) return set_err(SGM_ERR_INVALID, "bad timer / plan / slot");
   int st = ensure_ctx();
   if (st) return st;
@@ -748,11 +751,11 @@ int sgm_timer_enqueue(sgm_timer* t, int slot, sgm_plan* p, const void* const* in
   if (reps < 1) reps = 1;
   if ((st = plan_graph(p, inputs, outputs, rot))) return st;
   CUstream s = (CUstream)stream;
-  CU(D.cuGraphLaunch(p->gexec, s));  // warm-up (instruction cache, TMA descriptors)
+  for (int w = 0; w < warmup; ++w) CU(D.cuGraphLaunch(p->gexec, s));  // instruction cache, TMA descriptors
   CU(D.cuEventRecord(t->ev[2 * slot], s));
   for (int r = 0; r < reps; ++r) CU(D.cuGraphLaunch(p->gexec, s));
   CU(D.cuEventRecord(t->ev[2 * slot + 1], s));
-  g_launches += (long long)rot * (reps + 1);
+  g_launches += (long long)rot * (reps + (warmup > 0 ? warmup : 0));
   t->launches[slot] = rot * reps;
   if (slot > t->last) t->last = slot;
   return SGM_OK;

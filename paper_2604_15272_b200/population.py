@@ -237,12 +237,13 @@ class Timer:
         _abi.check(_abi.lib().sgm_timer_create(self.cap, C.byref(h)))
         self._h = h
 
-    def enqueue(self, slot: int, plan: Plan, input_sets, outputs, reps: int = 1) -> None:
+    def enqueue(self, slot: int, plan: Plan, input_sets, outputs, reps: int = 1, warmup: int = 1) -> None:
         import ctypes as C
         ip = _abi.ptr_array([t.data_ptr() for ins in input_sets for t in ins])
         op = _abi.ptr_array([t.data_ptr() for t in outputs])
         s = torch().cuda.current_stream(self.device).cuda_stream
-        _abi.check(_abi.lib().sgm_timer_enqueue(self._h, slot, plan._h, ip, op, len(input_sets), reps, C.c_void_p(s)))
+        _abi.check(_abi.lib().sgm_timer_enqueue(self._h, slot, plan._h, ip, op, len(input_sets), warmup, reps,
+                                                C.c_void_p(s)))
 
     def read(self, n: int) -> list:
         import ctypes as C
@@ -295,7 +296,9 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
                     _abi.check(L.sgm_compare_u32_acc(C.c_void_p(g.data_ptr()), C.c_void_p(e.data_ptr()), g.numel(),
                                                      stream, C.c_void_p(counters.data_ptr() + 8 * k)))
             plan = plans[k] = PLANS.get(u.cand, ctx.numsys, None, dev)
-            timer.enqueue(k, plan, [ctx.ws.sets[k % rot]], ctx.ws.outputs, reps=1)
+            # screening: one launch on its own input set (streams from HBM), no warm-up;
+            # it only ranks candidates for the rotation pass
+            timer.enqueue(k, plan, [ctx.ws.sets[k % rot]], ctx.ws.outputs, reps=1, warmup=0)
             rec.plan = {x: plan.info[x] for x in ("ctas", "cluster", "smem_bytes", "free_parts", "loop_parts",
                                                   "kernel_name", "summary")}
         except Exception as exc:  # recorded, the sweep goes on (failures are reported)
