@@ -605,7 +605,9 @@ struct Gen {
     // soft penalty (10 us per KB over) so the search can walk out of infeasible splits
     const double over = peak > cap ? (double)(peak - cap) / 1024.0 * 1e-5 : 0.0;
     // residency: two CTAs per SM when the tiles leave room for a 3 x 16 KB ring in half an SM
-    const bool two = prod && peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
+    // measured: the occupancy of kernels that use tcgen05 (TMEM) is one CTA per SM
+    // whatever their shared memory, so only CUDA-core kernels can pair up
+    const bool two = prod && !uses_tc() && peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
     const int cps = two ? 2 : 1;
     const i64 items = LB * FP * GP;
     const i64 slots = std::max<i64>(1, resident_ctas(CL, num_sms) * cps / CL);
@@ -795,6 +797,11 @@ struct Gen {
   }
   u32 loop_bits() const { return (LP > 1 && !loop_gs) ? (u32)(LP - 1) << loop_shift : 0; }
   bool class_gs(int c) const { return c >= 0 && cls[c].gsplit && cls[c].parts > 1; }
+  bool uses_tc() const {
+    for (auto& x : nodes)
+      if (x.kind == SGM_MATMUL && x.gemv && x.tc) return true;
+    return false;
+  }
 
   // pending partials + schedule
   // Partial values.  A node reducing a split class (matmul K, sum axis) yields a
@@ -1375,7 +1382,7 @@ struct Gen {
     i64 ctas = LB * FP * GP * CL;
     slotB = 32768;
     int S = std::min(6, (kSmemCap - base - 1024 - stg) / slotB);
-    if (ctas > num_sms) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM
+    if (ctas > num_sms && !uses_tc()) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM (no TMEM users)
       int S2 = (110 * 1024 - base - 1024 - stg) / 16384;
       if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); }
     }

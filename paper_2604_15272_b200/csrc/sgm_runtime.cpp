@@ -82,6 +82,7 @@ struct Driver {
   SGM_FN(cuModuleUnload, CUmodule)
   SGM_FN(cuModuleGetFunction, CUfunction*, CUmodule, const char*)
   SGM_FN(cuFuncSetAttribute, CUfunction, CUfunction_attribute, int)
+  SGM_FN(cuFuncGetAttribute, int*, CUfunction_attribute, CUfunction)
   SGM_FN(cuLaunchKernel, CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
          void**, void**)
   SGM_FN(cuMemAlloc, CUdeviceptr*, size_t)
@@ -137,6 +138,7 @@ struct Driver {
     g &= sym(cuModuleUnload, "cuModuleUnload");
     g &= sym(cuModuleGetFunction, "cuModuleGetFunction");
     g &= sym(cuFuncSetAttribute, "cuFuncSetAttribute");
+    g &= sym(cuFuncGetAttribute, "cuFuncGetAttribute");
     g &= sym(cuLaunchKernel, "cuLaunchKernel");
     g &= sym(cuMemAlloc, "cuMemAlloc_v2");
     g &= sym(cuMemFree, "cuMemFree_v2");
@@ -321,6 +323,8 @@ struct sgm_plan {
   CUdeviceptr scratch = 0;
   int numsys = 0;
   int64_t launch_ctas = 0;   // persistent grid: min(work CTAs, co-resident CTAs)
+  int occ_per_sm = 0;        // occupancy API: CTAs per SM (cluster 1)
+  int regs = 0, static_smem = 0;
   int n_in = 0, n_out = 0;
   size_t in_bytes[SGM_MAX_SLOTS] = {0};
   size_t out_bytes[SGM_MAX_SLOTS] = {0};
@@ -474,6 +478,17 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
       if (D.cuOccupancyMaxActiveBlocksPerMultiprocessor(&nb, p->fn, gr.threads, (size_t)gr.smem_bytes) == CUDA_SUCCESS &&
           nb > 0)
         resident = (int64_t)nb * g_dev[t_device].sms;
+      p->occ_per_sm = nb;
+      if (getenv("SGM_OCC_DEBUG"))
+        for (int kb : {16, 32, 48, 64, 80, 90, 96, 100, 104, 108, 112}) {
+          int n2 = 0;
+          D.cuOccupancyMaxActiveBlocksPerMultiprocessor(&n2, p->fn, gr.threads, (size_t)kb * 1024);
+          int n3 = 0;
+          D.cuOccupancyMaxActiveBlocksPerMultiprocessor(&n3, p->fn, 128, (size_t)kb * 1024);
+          fprintf(stderr, "occ: %d KB dyn -> %d CTAs/SM at %d threads, %d at 128 threads\n", kb, n2, gr.threads, n3);
+        }
+      D.cuFuncGetAttribute(&p->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, p->fn);
+      D.cuFuncGetAttribute(&p->static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, p->fn);
     }
     p->launch_ctas = gr.ctas;
     if (resident > 0 && resident < gr.ctas) p->launch_ctas = resident / gr.cluster * gr.cluster;
@@ -507,8 +522,8 @@ int sgm_plan_info_get(const sgm_plan* p, sgm_plan_info* info) {
   info->n_tcgen05 = p->gen.n_tcgen05;
   info->source_hash = sgmcg::fnv1a(p->gen.source);
   snprintf(info->kernel_name, sizeof info->kernel_name, "%s", p->gen.kernel_name.c_str());
-  snprintf(info->plan_summary, sizeof info->plan_summary, "grid=%lld %s", (long long)p->launch_ctas,
-           p->gen.summary.c_str());
+  snprintf(info->plan_summary, sizeof info->plan_summary, "grid=%lld occ=%d regs=%d sstat=%d %s",
+           (long long)p->launch_ctas, p->occ_per_sm, p->regs, p->static_smem, p->gen.summary.c_str());
   return SGM_OK;
 }
 
