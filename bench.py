@@ -402,13 +402,14 @@ def main() -> None:
             best[w] = {"error": "no valid candidate"}
             continue
         u = next(x for x in P.units(pops[w]) if x.index == win.index)
-        plan = PLANS.get(u.cand, ctx[w].numsys, None, local)
+        plan = PLANS.get(u.cand, ctx[w].numsys, {"variant": win.variant} if win.variant else None, local)
         lat = plan.time(ctx[w].ws.sets, ctx[w].ws.outputs, warmup=10, iters=args.best_iters)
         byts = P.algorithmic_bytes(pops[w])
         gbs = byts / (lat * 1e-6) / 1e9
         best[w] = {"latency_us": lat, "algorithmic_bytes": byts, "achieved_gbs": gbs, "frac_hbm": gbs / hbm,
                    "template": pops[w]["candidates"][u.pair]["template_id"], "mapping": u.cand.mapping_list(),
-                   "params": u.cand.params, "kernel": plan.kernel_name, "plan": plan.info["summary"],
+                   "params": u.cand.params, "variant": win.variant, "kernel": plan.kernel_name,
+                   "plan": plan.info["summary"],
                    "ctas": plan.info["ctas"], "cluster": plan.info["cluster"],
                    "ff_ok": win.ff_ok, "candidates": len(wrecs),
                    "failed": sum(1 for r in wrecs if r.error), "ff_mismatch": sum(1 for r in wrecs if r.ff_ok is False)}

@@ -121,7 +121,8 @@ typedef struct {
   int32_t use_tcgen05;     /* -1 off, 0 auto, 1 force where legal */
   int32_t no_tma;          /* 1: stream matmul operands with plain loads, no TMA producer warp */
   int32_t trace;           /* 1: record %globaltimer at schedule events (sgm_plan_trace) */
-  int32_t _reserved[7];
+  int32_t variant;         /* v > 0: the v-th best split the planner scored (physical-plan tuning) */
+  int32_t _reserved[6];
 } sgm_plan_hints;
 
 typedef struct {

@@ -659,7 +659,9 @@ struct Gen {
     for (auto& e : sched) cflush += e.type == Ev::FLUSH, gflush += e.type == Ev::GFLUSH;
     // fixed per-item work (activation loads, A^T builds, epilogues; measured 2-6 us) is
     // largely hidden when two CTAs share an SM
-    double t_item = (2.5e-6 + cflush * 5.0e-6 + gflush * 1.5e-6) * (two ? 0.4 : 1.0);
+    // fixed per-item costs measured with trace mode (tools/trace_one.py): ring refill
+    // + activation staging + epilogue ~4 us, cluster flush ~5 us, gsplit tail ~2 us
+    double t_item = (4.0e-6 + cflush * 5.0e-6 + gflush * 2.0e-6) * (two ? 0.4 : 1.0);
     double loop_iters = loop_begin_pos >= 0 ? (double)nloop / LP : 0.0;
     t_item += loop_iters * 0.6e-6;
     return t_stream + (double)rounds * t_item + over;
@@ -734,6 +736,7 @@ struct Gen {
       }
       if (next.empty()) break;
       std::sort(next.begin(), next.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (auto& ns : next) pool.push_back(ns);
       if (next.size() > 4) next.resize(4);
       const bool improved = next.front().first < best * 0.99;
       if (next.front().first < best) { best = next.front().first; best_st = next.front().second; }
@@ -745,15 +748,33 @@ struct Gen {
     return best;
   }
 
+  // every state the searches evaluated, for plan variants
+  std::vector<std::pair<double, PlanState>> pool;
+
   void split_plan() {
     PlanState best_st;
     double best = 1e30;
+    pool.clear();
     // gsplit-only first: cluster plans must win by 10% (their flush and GPC-placement
     // costs are the least well modelled, measured 3-7 us per item)
     for (int policy : {2, 1, 0}) {
       PlanState st;
       double c = greedy(policy, st);
       if (c < best * (policy == 2 ? 1.0 : 0.9)) { best = c; best_st = st; }
+    }
+    // hints.variant = v > 0: the v-th best distinct split the searches scored instead
+    // (the profiler auto-tunes the physical plan of the best candidates over variants)
+    if (d.hints.variant > 0) {
+      std::sort(pool.begin(), pool.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      std::vector<std::pair<double, PlanState>> uniq;
+      for (auto& ps : pool) {
+        bool dup = false;
+        for (auto& u : uniq) dup = dup || (u.second.parts == ps.second.parts && u.second.mode == ps.second.mode &&
+                                           u.second.lp == ps.second.lp && u.second.lmode == ps.second.lmode);
+        if (!dup) uniq.push_back(ps);
+        if ((int)uniq.size() > d.hints.variant) break;
+      }
+      if ((int)uniq.size() > d.hints.variant) { best = uniq[d.hints.variant].first; best_st = uniq[d.hints.variant].second; }
     }
     apply_state(best_st);
     bool valid;

@@ -168,6 +168,7 @@ class Record:
     pruned: bool = False
     refined: bool = False
     timing: str = ""
+    variant: int = 0
 
 
 class WorkloadContext:
@@ -264,7 +265,7 @@ class Timer:
 
 
 def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_factor: float = 2.0,
-                      refine_top: int = 3, refine_launches: int = 1000) -> list:
+                      refine_top: int = 3, refine_launches: int = 1000, variants: int = 6) -> list:
     """Evaluate candidates of one workload with no per-candidate host synchronisation.
 
     Pass 1 enqueues, per candidate, the finite-field run (outputs NaN-filled
@@ -272,8 +273,10 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
     timed launch (after one untimed launch, on its own input set, so it streams
     from HBM).  Pass 2 times one full rotation over the input sets (each launch
     misses L2) for the candidates within `screen_factor` of the pass-1 best.
-    Pass 3 re-times the `refine_top` fastest with `refine_launches` launches (the
-    paper's 1000-run protocol).  One host read per pass."""
+    Pass 3 tunes the physical plan of the `refine_top` fastest (planner variants
+    0..`variants`-1, one rotation each) and re-times each on its best variant with
+    `refine_launches` launches (the paper's 1000-run protocol).
+    One host read per pass."""
     import ctypes as C
     t = torch()
     dev = ctx.device
@@ -328,15 +331,38 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
             recs[k].latency_us = lat2[j]
             recs[k].timing = "rotation"
         top = sorted(sel, key=lambda k: (recs[k].latency_us, recs[k].index))[:refine_top]
+        # physical-plan tuning: planner variants of the top candidates (the FF check of
+        # the candidate covers every variant: each is the same block graph, re-split)
+        best_plan = {k: (recs[k].latency_us, 0, plans[k]) for k in top}
+        vp = []
+        for k in top:
+            for v in range(1, variants):
+                try:
+                    vp.append((k, v, PLANS.get(us[k].cand, ctx.numsys, {"variant": v}, dev)))
+                except Exception:
+                    pass
+        if vp:
+            timer = Timer(len(vp), dev)
+            for j, (k, v, pl) in enumerate(vp):
+                timer.enqueue(j, pl, ctx.ws.sets, ctx.ws.outputs, reps=1)
+            latv = timer.read(len(vp))
+            timer.close()
+            for j, (k, v, pl) in enumerate(vp):
+                if 0 < latv[j] < best_plan[k][0]:
+                    best_plan[k] = (latv[j], v, pl)
         timer = Timer(len(top), dev)
         for j, k in enumerate(top):
-            timer.enqueue(j, plans[k], ctx.ws.sets, ctx.ws.outputs, reps=max(1, -(-refine_launches // rot)))
+            timer.enqueue(j, best_plan[k][2], ctx.ws.sets, ctx.ws.outputs, reps=max(1, -(-refine_launches // rot)))
         lat3 = timer.read(len(top))
         timer.close()
         for j, k in enumerate(top):
             recs[k].latency_us = lat3[j]
             recs[k].timing = "refined"
             recs[k].refined = True
+            recs[k].variant = best_plan[k][1]
+            pl = best_plan[k][2]
+            recs[k].plan = {x: pl.info[x] for x in ("ctas", "cluster", "smem_bytes", "free_parts", "loop_parts",
+                                                    "kernel_name", "summary")}
     return recs
 
 

@@ -28,14 +28,16 @@ def main():
         rs = [r for r in recs if r["workload"] == w and r["latency_us"] and not r.get("error")]
         r = min(rs, key=lambda r: r["latency_us"])
         u = us[r["index"]]
+        variant = r.get("variant", 0)
     else:
         params = json.loads(sys.argv[3])
         want = sorted(mapping.split(","))
         u = next(x for x in us if x.cand.mapping_list() == want and x.cand.params == params)
+        variant = 0
     torch.cuda.set_device(0)
     _abi.bind_device(0)
     ns = _abi.FF if "--ff" in sys.argv else P.numsys_of(pop["dtype"])
-    plan = PLANS.get(u.cand, ns, None, 0)
+    plan = PLANS.get(u.cand, ns, {"variant": variant} if variant else None, 0)
     ws = workspace(u.cand.program, ns, 0)
     print(f"{w} {u.cand.mapping_list()} {u.cand.params} kernel={plan.kernel_name} {plan.info['summary']}", flush=True)
     for i in range(iters):

@@ -41,17 +41,19 @@ def pick(w, mapping, arg):
     if mapping == "best":
         recs = [r for r in json.load(open(arg)) if r["workload"] == w and r.get("latency_us") and not r.get("error")]
         r = min(recs, key=lambda r: r["latency_us"])
-        return pop, us[r["index"]]
+        return pop, us[r["index"]], r.get("variant", 0)
     params = json.loads(arg)
     want = sorted(mapping.split(","))
-    return pop, next(x for x in us if x.cand.mapping_list() == want and x.cand.params == params)
+    return pop, next(x for x in us if x.cand.mapping_list() == want and x.cand.params == params), 0
 
 
 def main():
     w, mapping, arg = sys.argv[1:4]
     hints = json.loads(sys.argv[4]) if len(sys.argv) > 4 else {}
     hints["trace"] = 1
-    pop, u = pick(w, mapping, arg)
+    pop, u, variant = pick(w, mapping, arg)
+    if variant and "variant" not in hints:
+        hints["variant"] = variant
     torch.cuda.set_device(0)
     _abi.bind_device(0)
     ns = P.numsys_of(pop["dtype"])
