@@ -846,6 +846,15 @@ struct Gen {
     }
   }
 
+  // bytes a node streams from HBM (view operands of a matmul)
+  i64 stream_bytes(const Node& x) const {
+    if (x.kind != SGM_MATMUL) return 0;
+    i64 b = 0;
+    for (int k = 0; k < 2; ++k)
+      if (nodes[x.in[k]].store == ST_VIEW) b += prod4(nodes[x.in[k]].sl) * es;
+    return b;
+  }
+
   void reduce_bits(Node& x) const {
     if (x.kind == SGM_MATMUL) {
       int c = nodes[x.in[0]].cls[3];
@@ -922,8 +931,34 @@ struct Gen {
           if (all_lin && pending.count(p)) pending.erase(p);
         }
     };
-    for (int n = 0; n < (int)nodes.size(); ++n)
-      if (nodes[n].hoist) push_node(n);
+    // Within each region nodes are list-scheduled by height (longest chain to a sink):
+    // a short dependent chain of small matmuls (LoRA's X@A -> T@B) runs before an
+    // independent big stream (X@W), so its latency hides under the stream, whose boxes
+    // the producer then issues back to back.
+    std::vector<int> height(nodes.size(), 0);
+    for (int n = (int)nodes.size() - 1; n >= 0; --n)
+      for (int c : nodes[n].cons) height[n] = std::max(height[n], height[c] + 1);
+    auto push_region = [&](auto in_region) {
+      std::vector<char> done(nodes.size(), 0);
+      for (int n = 0; n < (int)nodes.size(); ++n) done[n] = !in_region(n);
+      for (;;) {
+        int pick = -1;
+        for (int n = 0; n < (int)nodes.size(); ++n) {
+          if (done[n]) continue;
+          bool ready = true;
+          for (int k = 0; k < nodes[n].nin; ++k) ready = ready && (done[nodes[n].in[k]] || !in_region(nodes[n].in[k]));
+          // in-region inputs must already be scheduled (done marks both out-of-region and scheduled)
+          if (!ready) continue;
+          if (pick < 0 || height[n] > height[pick] ||
+              (height[n] == height[pick] && stream_bytes(nodes[n]) < stream_bytes(nodes[pick])))
+            pick = n;
+        }
+        if (pick < 0) break;
+        done[pick] = 1;
+        push_node(pick);
+      }
+    };
+    push_region([&](int n) { return (bool)nodes[n].hoist; });
     bool has_loop = false;
     for (auto& x : nodes) has_loop = has_loop || (x.body && !x.hoist);
     if (has_loop) {
@@ -932,8 +967,7 @@ struct Gen {
       b.type = Ev::LOOP_BEGIN;
       loop_begin_pos = (int)sched.size();
       sched.push_back(b);
-      for (int n = 0; n < (int)nodes.size(); ++n)
-        if (nodes[n].body && !nodes[n].hoist) push_node(n);
+      push_region([&](int n) { return nodes[n].body && !nodes[n].hoist; });
       Ev en;
       en.type = Ev::LOOP_END;
       loop_end_pos = (int)sched.size();
@@ -941,8 +975,7 @@ struct Gen {
     } else {
       loop_begin_pos = loop_end_pos = -1;
     }
-    for (int n = 0; n < (int)nodes.size(); ++n)
-      if (!nodes[n].body) push_node(n);
+    push_region([&](int n) { return !nodes[n].body; });
   }
 
   // A gsplit plan is legal iff its partials are reduced by a single GFLUSH after

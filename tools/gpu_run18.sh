@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -8 gpurun_out/pytest_gpu.log
+timeout 1200 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --records gpurun_out/records.json > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc $?"
+tail -3 gpurun_out/bench.err
+python tools/best.py gpurun_out/records.json 2
+for W in L A G R Q; do timeout 300 python tools/trace_one.py $W best gpurun_out/records.json 2>&1 | head -24 | cut -c1-200; done
