@@ -122,7 +122,8 @@ typedef struct {
   int32_t no_tma;          /* 1: stream matmul operands with plain loads, no TMA producer warp */
   int32_t trace;           /* 1: record %globaltimer at schedule events (sgm_plan_trace) */
   int32_t variant;         /* v > 0: the v-th best split the planner scored (physical-plan tuning) */
-  int32_t _reserved[6];
+  int32_t one_cta;         /* 1: size the TMA ring for one CTA per SM (32 KB slots) */
+  int32_t _reserved[5];
 } sgm_plan_hints;
 
 typedef struct {

@@ -607,7 +607,7 @@ struct Gen {
     // residency: two CTAs per SM when the tiles leave room for a 3 x 16 KB ring in half an SM
     // measured: the occupancy of kernels that use tcgen05 (TMEM) is one CTA per SM
     // whatever their shared memory, so only CUDA-core kernels can pair up
-    const bool two = prod && !uses_tc() && peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
+    const bool two = prod && !uses_tc() && !d.hints.one_cta && peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
     const int cps = two ? 2 : 1;
     const i64 items = LB * FP * GP;
     const i64 slots = std::max<i64>(1, resident_ctas(CL, num_sms) * cps / CL);
@@ -1436,7 +1436,7 @@ struct Gen {
     i64 ctas = LB * FP * GP * CL;
     slotB = 32768;
     int S = std::min(6, (kSmemCap - base - 1024 - stg) / slotB);
-    if (ctas > num_sms && !uses_tc()) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM (no TMEM users)
+    if (ctas > num_sms && !uses_tc() && !d.hints.one_cta) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM (no TMEM users)
       int S2 = (110 * 1024 - base - 1024 - stg) / 16384;
       if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); }
     }

@@ -127,6 +127,7 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.no_tma = int(h.get("no_tma", 0))
     d.hints.trace = int(h.get("trace", 0))
     d.hints.variant = int(h.get("variant", 0))
+    d.hints.one_cta = int(h.get("one_cta", 0))
     return d
 
 

@@ -169,6 +169,7 @@ class Record:
     refined: bool = False
     timing: str = ""
     variant: int = 0
+    hints: dict = field(default_factory=dict)
 
 
 class WorkloadContext:
@@ -265,7 +266,7 @@ class Timer:
 
 
 def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_factor: float = 2.0,
-                      refine_top: int = 3, refine_launches: int = 1000, variants: int = 6) -> list:
+                      refine_top: int = 3, refine_launches: int = 1000, variants: int = 1) -> list:
     """Evaluate candidates of one workload with no per-candidate host synchronisation.
 
     Pass 1 enqueues, per candidate, the finite-field run (outputs NaN-filled
@@ -364,6 +365,41 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
             recs[k].plan = {x: pl.info[x] for x in ("ctas", "cluster", "smem_bytes", "free_parts", "loop_parts",
                                                     "kernel_name", "summary")}
     return recs
+
+
+VARIANT_HINTS = [{}] + [{"variant": v} for v in range(1, 6)] + [{"one_cta": 1}] + \
+    [{"one_cta": 1, "variant": v} for v in range(1, 4)]
+
+
+def tune_physical(ctx: "WorkloadContext", u: Unit, launches: int = 1000) -> tuple:
+    """Physical-plan tuning of one candidate: time each planner variant (other scored
+    splits, one-CTA-per-SM rings) over one rotation, re-time the fastest with
+    `launches` launches.  Returns (latency_us, hints, plan).  The candidate's FF
+    verdict covers every variant: the block graph is the same, re-split."""
+    dev = ctx.device
+    plans = []
+    for h in VARIANT_HINTS:
+        try:
+            plans.append((h, PLANS.get(u.cand, ctx.numsys, h or None, dev)))
+        except Exception:
+            pass
+    seen, uniq = set(), []
+    for h, p in plans:  # variants that generate the same kernel are timed once
+        if p.kernel_name not in seen:
+            seen.add(p.kernel_name)
+            uniq.append((h, p))
+    timer = Timer(len(uniq), dev)
+    for j, (h, p) in enumerate(uniq):
+        timer.enqueue(j, p, ctx.ws.sets, ctx.ws.outputs, reps=2)
+    lat = timer.read(len(uniq))
+    timer.close()
+    j = min(range(len(uniq)), key=lambda k: lat[k] if lat[k] > 0 else 1e30)
+    h, p = uniq[j]
+    timer = Timer(1, dev)
+    timer.enqueue(0, p, ctx.ws.sets, ctx.ws.outputs, reps=max(1, -(-launches // ctx.ws.rot)))
+    best = timer.read(1)[0]
+    timer.close()
+    return best, h, p
 
 
 def argmin(records: list) -> Optional[Record]:

@@ -118,7 +118,7 @@ def test_best_kernels_deployment_dtype(S):
         ins = {t["name"]: _round(rng.standard_normal(tuple(t["dims"])), dt) for t in prog["tensors"]
                if t["role"] == "input"}
         exp = block_np.run_program(prog, ins)
-        hints = {"variant": b["variant"]} if b.get("variant") else None
+        hints = b.get("hints") or None
         got = S.run_concrete(u.cand, ins, dtype=dt, hints=hints)
         for name in prog["outputs"]:
             assert S.rel_err(got[name], exp[name]) < TOL[dt], w

@@ -23,21 +23,27 @@ def main():
     iters = int(sys.argv[sys.argv.index("--iters") + 1]) if "--iters" in sys.argv else 20
     pop = P.load_population(w)
     us = P.units(pop)
-    if mapping == "best":
+    if mapping == "best" and isinstance(json.load(open(sys.argv[3])), dict):  # bench --best-out file
+        b = json.load(open(sys.argv[3]))[w]
+        u = next(x for x in us if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"])
+        variant = b.get("hints") or {}
+    elif mapping == "best":
         recs = json.load(open(sys.argv[3]))
         rs = [r for r in recs if r["workload"] == w and r["latency_us"] and not r.get("error")]
         r = min(rs, key=lambda r: r["latency_us"])
         u = us[r["index"]]
-        variant = r.get("variant", 0)
+        variant = r.get("hints") or ({"variant": r["variant"]} if r.get("variant") else {})
     else:
         params = json.loads(sys.argv[3])
         want = sorted(mapping.split(","))
         u = next(x for x in us if x.cand.mapping_list() == want and x.cand.params == params)
-        variant = 0
+        variant = {}
+    if len(sys.argv) > 4 and sys.argv[4].startswith("{"):
+        variant = json.loads(sys.argv[4])
     torch.cuda.set_device(0)
     _abi.bind_device(0)
     ns = _abi.FF if "--ff" in sys.argv else P.numsys_of(pop["dtype"])
-    plan = PLANS.get(u.cand, ns, {"variant": variant} if variant else None, 0)
+    plan = PLANS.get(u.cand, ns, variant or None, 0)
     ws = workspace(u.cand.program, ns, 0)
     print(f"{w} {u.cand.mapping_list()} {u.cand.params} kernel={plan.kernel_name} {plan.info['summary']}", flush=True)
     for i in range(iters):

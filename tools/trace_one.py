@@ -38,10 +38,14 @@ def name(ev: int) -> str:
 def pick(w, mapping, arg):
     pop = P.load_population(w)
     us = P.units(pop)
+    if mapping == "best" and isinstance(json.load(open(arg)), dict):  # bench --best-out file
+        b = json.load(open(arg))[w]
+        u = next(x for x in us if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"])
+        return pop, u, b.get("hints") or {}
     if mapping == "best":
         recs = [r for r in json.load(open(arg)) if r["workload"] == w and r.get("latency_us") and not r.get("error")]
         r = min(recs, key=lambda r: r["latency_us"])
-        return pop, us[r["index"]], r.get("variant", 0)
+        return pop, us[r["index"]], r.get("hints") or ({"variant": r["variant"]} if r.get("variant") else {})
     params = json.loads(arg)
     want = sorted(mapping.split(","))
     return pop, next(x for x in us if x.cand.mapping_list() == want and x.cand.params == params), 0
@@ -52,8 +56,8 @@ def main():
     hints = json.loads(sys.argv[4]) if len(sys.argv) > 4 else {}
     hints["trace"] = 1
     pop, u, variant = pick(w, mapping, arg)
-    if variant and "variant" not in hints:
-        hints["variant"] = variant
+    for k, v in (variant or {}).items():
+        hints.setdefault(k, v)
     torch.cuda.set_device(0)
     _abi.bind_device(0)
     ns = P.numsys_of(pop["dtype"])
