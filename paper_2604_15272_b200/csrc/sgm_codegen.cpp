@@ -701,6 +701,7 @@ struct Gen {
         if (!seen.insert(key(st)).second) return;
         apply_state(st);
         if (LB * FP * GP > (1LL << 22) || CL > max_cluster) return;
+        if (d.hints.max_gsplit > 0 && GP > d.hints.max_gsplit) return;
         bool ok;
         double c = plan_cost(&ok);
         if (dbg)
