@@ -100,6 +100,7 @@ struct Node {
   int tma_id = -1;
   int kc = 64;       // rows of B per ring stage
   int bw = 64;       // columns of B per TMA box (fp32 path)
+  int acc = 1;       // TMEM accumulators per 128-column tile (tcgen05 path)
   bool staged = false;     // loader tile fetched by the producer (TMA) into a staging buffer
   int stage_id = -1, stage_off = 0, sbox = 0;
   bool inv = false;        // item-invariant: computed once per CTA, before the item loop
@@ -1094,8 +1095,12 @@ struct Gen {
             x.xb_shared = x.sl[0] * x.sl[1] == 1;
             x.at_bytes = x.xb_shared ? 0 : 32 * K;
             x.red_bytes = 0;
+            // independent accumulators (up to 4 per tile, TMEM permitting): consecutive MMAs
+            // of a stage rotate over them instead of serialising on one
+            x.acc = 4;
+            while (x.acc > 1 && ntl * x.acc * 16 > 512) x.acc /= 2;
             int cols = 32;
-            while (cols < ntl * 16) cols *= 2;
+            while (cols < ntl * x.acc * 16) cols *= 2;
             x.tc_cols = cols;
           } else if (ns == SGM_F32 && M <= 8 && K % 8 == 0 && NN % 8 == 0 && (d3 * 4) % 16 == 0) {
             x.tma = true;
@@ -1801,7 +1806,7 @@ struct Gen {
         if (x.tma && x.tc) {
           os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS << ", "
-             << slotB << ", NT, " << (x.xb_build ? "true" : "false") << ">(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
+             << slotB << ", NT, " << (x.xb_build ? "true" : "false") << ", " << x.acc << ">(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
              << ", tmem_base, ring, full, empty, done, sq, sdph);\n";
         } else if (x.tma) {
           os << "    sgm::mm_stream_f32<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "

@@ -785,8 +785,13 @@ __device__ __forceinline__ void build_xb(u16* __restrict__ xb, const float* __re
 
 // BUILD = false: the caller already built xbuf (shared A operand, or an
 // item-invariant one built once per CTA); requires B0 * B1 == 1.
+// ACC independent accumulators per tile (TMEM columns (t*ACC + a)*16): MMAs into
+// one accumulator serialise on its read-modify-write, and with N = 16 an MMA is
+// only ~8 issue cycles, so a long K chain of a single 128-column tile (attention's
+// P@V) is latency-bound; consecutive MMAs rotate over the accumulators instead
+// and the epilogue adds them.
 template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int SLOT, int NT,
-          bool BUILD = true>
+          bool BUILD = true, int ACC = 1>
 __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const float* __restrict__ A,
                                              unsigned char* __restrict__ xbuf, u32 tmem, unsigned char* ring, u64* full,
                                              u64* empty, u64* done, u32& q, u32& dph) {
@@ -794,7 +799,10 @@ __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const floa
   constexpr int NKC = K / KC;
   constexpr bool SPLIT = M <= 8;
   constexpr u32 IDESC = UMMA_IDESC_BF16_M128_N16;
-  static_assert(K % KC == 0 && KC % 16 == 0 && KC * 256 <= SLOT && M <= 16 && NTL * 16 <= 512, "mm_stream_tc shape");
+  constexpr int NMMA = K / 16;                      // MMAs per tile
+  constexpr int AC = ACC < NMMA ? ACC : NMMA;        // accumulators actually written
+  static_assert(K % KC == 0 && KC % 16 == 0 && KC * 256 <= SLOT && M <= 16 && NTL * ACC * 16 <= 512,
+                "mm_stream_tc shape");
   static_assert(BUILD || B0 * B1 == 1, "a prebuilt A^T covers one batch");
   u16* xb = reinterpret_cast<u16*>(xbuf);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -820,7 +828,8 @@ __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const floa
           for (int ks = 0; ks < KC / 16; ++ks) {
             const u64 ad = umma_desc_sw128(st + ks * 2048, KC * 128, 1024);
             const u64 bd = umma_desc(xs + ((kc * KC + ks * 16) >> 3) * 256, 256, 128);
-            umma_bf16(tmem + t * 16, ad, bd, IDESC, (kc | ks) != 0);
+            const int g = kc * (KC / 16) + ks;  // MMA index along K
+            umma_bf16(tmem + (t * ACC + g % AC) * 16, ad, bd, IDESC, g >= AC);
           }
           umma_commit(&empty[slot]);
         }
@@ -831,14 +840,20 @@ __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const floa
     dph ^= 1u;
     tc_fence_after();
     for (int t = warp >> 2; t < NTL; t += NT / 128) {
-      u32 v[16];
-      tmem_ld16(tmem + ((u32)((warp & 3) * 32) << 16) + t * 16, v);
+      float acc[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
+#pragma unroll
+      for (int a = 0; a < AC; ++a) {
+        u32 v[16];
+        tmem_ld16(tmem + ((u32)((warp & 3) * 32) << 16) + (t * ACC + a) * 16, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] += __uint_as_float(v[i]);
+      }
       const int n = t * 128 + (warp & 3) * 32 + lane;
       if (n < NN) {
 #pragma unroll
-        for (int m = 0; m < M; ++m)
-          out[((i64)bi * M + m) * NN + n] = SPLIT ? __uint_as_float(v[m]) + __uint_as_float(v[8 + m])
-                                                  : __uint_as_float(v[m]);
+        for (int m = 0; m < M; ++m) out[((i64)bi * M + m) * NN + n] = SPLIT ? acc[m] + acc[8 + m] : acc[m];
       }
     }
     tc_fence_before();
