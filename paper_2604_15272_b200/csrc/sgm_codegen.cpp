@@ -1571,9 +1571,11 @@ struct Gen {
   }
 
   void emit_producer() {
-    // wait for the compute warps' item-invariant prologue (its loads would queue
-    // behind a full ring of TMA traffic otherwise)
-    os << "    if (tid == NT) {\n      unsigned pq = 0;\n      sgm::mbar_wait(go, 0);\n";
+    // the producer fills the ring while the compute warps run the item-invariant
+    // prologue (measured: a few % faster than holding it back so the prologue's
+    // loads do not queue behind TMA traffic; SGM_LATE_STREAM=1 restores the wait)
+    os << "    if (tid == NT) {\n      unsigned pq = 0;\n";
+    if (getenv("SGM_LATE_STREAM")) os << "      sgm::mbar_wait(go, 0);\n";
     os << "      unsigned pit = 0;\n";
     os << "      for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl, ++pit) {\n";
     emit_item_vars("      ");
@@ -1662,6 +1664,7 @@ struct Gen {
   void emit_flush(const std::vector<int>& fl, int pos) {
     // reduce-scatter (DSMEM loads into tmp) + all-gather (DSMEM stores)
     os << cl_sync();
+    os << "  SGM_TR(" << 3000 + 4 * pos + 1 << ");\n";
     for (int f : fl) {
       const Node& x = nodes[f];
       u32 keep = (u32)(CL - 1) & ~x.pend;
@@ -1669,6 +1672,7 @@ struct Gen {
          << ", (C*)(sm + " << flush_tmp_off.at({pos, f}) << "), crank);\n";
     }
     os << cl_sync();
+    os << "  SGM_TR(" << 3000 + 4 * pos + 2 << ");\n";
     for (int f : fl) {
       const Node& x = nodes[f];
       u32 keep = (u32)(CL - 1) & ~x.pend;
@@ -1676,6 +1680,7 @@ struct Gen {
          << ", (const C*)(sm + " << flush_tmp_off.at({pos, f}) << "), crank);\n";
     }
     os << cl_sync();
+    os << "  SGM_TR(" << 3000 + 4 * pos + 3 << ");\n";
   }
 
   // gsplit tail reduction: every work item of a group stores its partial tiles to
@@ -1683,7 +1688,7 @@ struct Gen {
   // part order (bit-identical whatever the arrival order), resets the counter
   // and runs the rest of the item; the others go on to their next item.
   i64 gws_off = 0, gcnt_off = 0, gws_tile = 0, gws_end = 0;
-  void emit_gflush(const std::vector<int>& fl) {
+  void emit_gflush(const std::vector<int>& fl, int gpos) {
     i64 fo[SGM_MAX_NODES];
     i64 tot = 0;
     for (int f : fl) { fo[f] = tot; tot += prod4(nodes[f].sl); }
@@ -1699,6 +1704,7 @@ struct Gen {
     os << "      sgm::csync<NT>();\n";
     os << "      if (tid == 0) sgm_last = (sgm::atom_add_acq_rel(&gcnt[grp], 1u) == " << GP - 1 << "u);\n";
     os << "      sgm::csync<NT>();\n    }\n";
+    os << "  SGM_TR(" << 3000 + 4 * gpos + 1 << ");\n";
     os << "  if (sgm_last) {\n";
     os << "    {\n      const C* gw = (const C*)((unsigned char*)a.scratch + " << gws_off << "LL);\n";
     for (int f : fl)
@@ -1707,6 +1713,7 @@ struct Gen {
          << " + e])); " << tile_ptr(f) << "[e] = N::fin(acc); }\n";
     os << "      if (tid == 0) ((unsigned*)((unsigned char*)a.scratch + " << gcnt_off << "LL))[grp] = 0u;\n";
     os << "      sgm::csync<NT>();\n    }\n";
+    os << "  SGM_TR(" << 3000 + 4 * gpos + 2 << ");\n";
   }
 
   void emit_node(int n, bool in_loop) {
@@ -1939,6 +1946,7 @@ struct Gen {
       os << "  __shared__ unsigned tmem_slot;\n";
       os << "  const unsigned tmem_base = sgm::tmem_alloc<NT>(&tmem_slot, " << tmem_cols << "u);\n";
     }
+    os << "  SGM_TR(8);\n";
     {
       bool any = false;
       for (int p = 0; p < (int)sched.size(); ++p)
@@ -1947,6 +1955,7 @@ struct Gen {
           any = true;
           emit_node(sched[p].node, false);
         }
+      if (any) os << "  SGM_TR(9);\n";
       for (auto& x : nodes) {
         if (!(x.kind == SGM_MATMUL && x.tma && x.tc && x.xb_shared)) continue;
         const Node& a = nodes[x.in[0]];
@@ -1989,11 +1998,24 @@ struct Gen {
         emit_flush(e.flush, p);
       } else if (e.type == Ev::GFLUSH) {
         os << "  SGM_TR(" << 2000 + p << ");\n";
-        emit_gflush(e.flush);
+        emit_gflush(e.flush, p);
         gs_open = true;
       } else if (!nodes[e.node].inv) {
         if (nodes[e.node].kind == SGM_MATMUL || nodes[e.node].kind == SGM_SUM) os << "  SGM_TR(" << 1000 + e.node << ");\n";
-        emit_node(e.node, in_loop);
+        if (d.hints.trace) {  // thread 0's own share done (before the node's closing barrier)
+          std::ostringstream keep;
+          keep << os.str();
+          os.str("");
+          emit_node(e.node, in_loop);
+          std::string body = os.str();
+          const std::string tail = "    sgm::csync<NT>();\n";
+          if (body.size() > tail.size() && body.compare(body.size() - tail.size(), tail.size(), tail) == 0)
+            body.insert(body.size() - tail.size(), "  SGM_TR(" + std::to_string(1500 + e.node) + ");\n");
+          os.str("");
+          os << keep.str() << body;
+        } else {
+          emit_node(e.node, in_loop);
+        }
       }
     }
     if (gs_open) os << "  }  // last work item of the reduction group\n";

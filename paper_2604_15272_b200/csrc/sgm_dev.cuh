@@ -229,16 +229,34 @@ __device__ __forceinline__ void load_tile(typename N::C* __restrict__ dst, const
   typedef typename N::S S;
   constexpr int ROWS = D0 * D1 * D2;
   if constexpr (VEC > 1) {
+    // batches of up to 8 independent 16-byte loads per thread in flight (a cold
+    // prologue load is latency-bound, not bandwidth-bound)
     constexpr int V3 = D3 / VEC;
-    for (int e = threadIdx.x; e < ROWS * V3; e += NT) {
-      const int v = e % V3;
-      const int r = e / V3;
-      const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
-      const S* p = src + i0 * S0 + i1 * S1 + i2 * S2 + (i64)v * VEC;
-      union { uint4 q; S s[VEC]; } u;
-      u.q = *reinterpret_cast<const uint4*>(p);
+    constexpr int TOT = ROWS * V3;
+    constexpr int IT = (TOT + NT - 1) / NT;
+    constexpr int BT = IT < 8 ? IT : 8;
+    for (int b = 0; b < IT; b += BT) {
+      union U { uint4 q; S s[VEC]; } u[BT];
 #pragma unroll
-      for (int t = 0; t < VEC; ++t) dst[r * D3 + v * VEC + t] = N::ld(u.s[t]);
+      for (int j = 0; j < BT; ++j) {
+        const int e = threadIdx.x + (b + j) * NT;
+        if (b + j < IT && e < TOT) {
+          const int v = e % V3;
+          const int r = e / V3;
+          const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
+          u[j].q = *reinterpret_cast<const uint4*>(src + i0 * S0 + i1 * S1 + i2 * S2 + (i64)v * VEC);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < BT; ++j) {
+        const int e = threadIdx.x + (b + j) * NT;
+        if (b + j < IT && e < TOT) {
+          const int v = e % V3;
+          const int r = e / V3;
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) dst[r * D3 + v * VEC + t] = N::ld(u[j].s[t]);
+        }
+      }
     }
   } else {
     for (int e = threadIdx.x; e < ROWS * D3; e += NT) {
@@ -585,6 +603,9 @@ template <int NT> __device__ __forceinline__ void tmem_free(u32 base, u32 ncols)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(ncols) : "memory");
 }
 
+template <int M, int K, i64 SA2, i64 SA3, int NT>
+__device__ __forceinline__ void build_xb(u16* __restrict__ xb, const float* __restrict__ Ab);
+
 template <int NN, int K, int KC, int S> struct gemv_tc_layout {
   static constexpr int NTL = (NN + 127) / 128;     // 128-column tiles
   static constexpr int STAGE = (KC / 8) * 2048;    // one (k-chunk, tile) stage
@@ -614,18 +635,7 @@ __device__ __forceinline__ void mm_gemv_tc(float* __restrict__ out, const float*
     const int b1 = bi % B1, b0 = bi / B1;
     const float* Ab = A + b0 * SA0 + b1 * SA1;
     const u16* Bb = B + b0 * SB0 + b1 * SB1;
-    // A^T, K-major canonical: rows 0..M-1 = bf16(a); rows 8..8+M-1 = bf16(a - hi) when SPLIT
-    for (int e = tid; e < 16 * K; e += NT) {
-      const int kk = e & 7, m = (e >> 3) & 15, k = (e >> 7) * 8 + kk;
-      u16 v = 0;
-      if (m < M) {
-        v = NBF16::st(Ab[(i64)m * SA2 + (i64)k * SA3]);
-      } else if (SPLIT && m >= 8 && m - 8 < M) {
-        const float a = Ab[(i64)(m - 8) * SA2 + (i64)k * SA3];
-        v = NBF16::st(a - NBF16::ld(NBF16::st(a)));
-      }
-      xb[e] = v;
-    }
+    build_xb<M, K, SA2, SA3, NT>(xb, Ab);  // A^T, K-major canonical (see build_xb)
     fence_async_smem();
     if (tid == 0) {
       for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
@@ -754,9 +764,65 @@ __device__ __forceinline__ u64 umma_desc_sw128(u32 saddr, u32 lbo, u32 sbo) {
 // A^T of one batch as the K-major no-swizzle MMA B operand (16 rows x K, bf16):
 // core matrix (k8, m) = 8 consecutive k of row m at byte (k8*16 + m)*16; rows
 // 8.. hold the bf16 residual a - bf16(a) when M <= 8 (16 mantissa bits overall).
+//
+// Fast path (row-major A, K % 32 == 0): a warp converts 4 k8 x 8 rows per step.
+// It reads with lane = (m, j) and the two 16-byte halves of each 32-byte chunk
+// in an order alternating with m, so each 8-lane phase of an LDS.128 touches 8
+// distinct bank groups; shuffles transpose to lane = (j, m) so each phase of the
+// STS.128 writes one contiguous 128-byte core matrix (both sides conflict-free;
+// a direct (k8, m) walk is an 8-way read conflict with rows K*4 bytes apart).
 template <int M, int K, i64 SA2, i64 SA3, int NT>
 __device__ __forceinline__ void build_xb(u16* __restrict__ xb, const float* __restrict__ Ab) {
   constexpr bool SPLIT = M <= 8;
+  if constexpr (SA3 == 1 && K % 32 == 0 && M <= 16) {
+    constexpr int NW = NT / 32;
+    constexpr int MG = SPLIT ? 1 : 2;  // row groups of 8 read from A
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rm = lane >> 2, rj = lane & 3, h0 = rm & 1;
+    const int src_lane = ((lane & 7) << 2) | (lane >> 3);
+    const int wm = lane & 7, wj = lane >> 3;
+    for (int it = warp; it < K / 32; it += NW) {
+#pragma unroll
+      for (int g = 0; g < MG; ++g) {
+        const int m = g * 8 + rm;
+        float a[8];
+        if (m < M) {
+          const float* p = Ab + (i64)m * SA2 + (it * 4 + rj) * 8;
+          const float4 x0 = *reinterpret_cast<const float4*>(p + 4 * h0);
+          const float4 x1 = *reinterpret_cast<const float4*>(p + 4 * (h0 ^ 1));
+          const float4 lo4 = h0 ? x1 : x0, hi4 = h0 ? x0 : x1;
+          a[0] = lo4.x; a[1] = lo4.y; a[2] = lo4.z; a[3] = lo4.w; a[4] = hi4.x; a[5] = hi4.y; a[6] = hi4.z; a[7] = hi4.w;
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) a[kk] = 0.0f;
+        }
+        u32 hv[4], lv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const u16 h_0 = NBF16::st(a[2 * i]), h_1 = NBF16::st(a[2 * i + 1]);
+          hv[i] = (u32)h_0 | ((u32)h_1 << 16);
+          if constexpr (SPLIT) {
+            const u16 l_0 = NBF16::st(a[2 * i] - NBF16::ld(h_0)), l_1 = NBF16::st(a[2 * i + 1] - NBF16::ld(h_1));
+            lv[i] = (u32)l_0 | ((u32)l_1 << 16);
+          }
+        }
+        uint4 w;
+        w.x = __shfl_sync(0xffffffffu, hv[0], src_lane);
+        w.y = __shfl_sync(0xffffffffu, hv[1], src_lane);
+        w.z = __shfl_sync(0xffffffffu, hv[2], src_lane);
+        w.w = __shfl_sync(0xffffffffu, hv[3], src_lane);
+        const int k8 = it * 4 + wj;
+        *reinterpret_cast<uint4*>(xb + (i64)(k8 * 16 + g * 8 + wm) * 8) = w;
+        if constexpr (SPLIT) {
+          w.x = __shfl_sync(0xffffffffu, lv[0], src_lane);
+          w.y = __shfl_sync(0xffffffffu, lv[1], src_lane);
+          w.z = __shfl_sync(0xffffffffu, lv[2], src_lane);
+          w.w = __shfl_sync(0xffffffffu, lv[3], src_lane);
+          *reinterpret_cast<uint4*>(xb + (i64)(k8 * 16 + 8 + wm) * 8) = w;
+        }
+      }
+    }
+  } else {
   for (int c = threadIdx.x; c < 2 * K; c += NT) {  // (k8, m) chunks of 8 elements
     const int m = c & 15, k8 = c >> 4;
     union { uint4 q; u16 h[8]; } u;
@@ -780,6 +846,7 @@ __device__ __forceinline__ void build_xb(u16* __restrict__ xb, const float* __re
       }
     }
     *reinterpret_cast<uint4*>(xb + (i64)c * 8) = u.q;
+  }
   }
 }
 

@@ -28,11 +28,16 @@ from paper_2604_15272_b200.tuner import workspace  # noqa: E402
 def name(ev: int) -> str:
     if ev >= 4000:
         return f"P:stream n{ev - 4000}"
+    if ev >= 3000:
+        return f"fl@{(ev - 3000) // 4}.{(ev - 3000) % 4}"
     if ev >= 2000:
         return f"flush@{ev - 2000}"
+    if ev >= 1500:
+        return f"own n{ev - 1500}"
     if ev >= 1000:
         return f"node n{ev - 1000}"
-    return {0: "entry", 1: "start", 2: "item", 3: "P:item", 5: "item end", 6: "P:done", 7: "exit"}.get(ev, str(ev))
+    return {0: "entry", 1: "start", 2: "item", 3: "P:item", 5: "item end", 6: "P:done", 7: "exit", 8: "tmem",
+            9: "invariants"}.get(ev, str(ev))
 
 
 def pick(w, mapping, arg):
@@ -75,6 +80,7 @@ def main():
     comp = defaultdict(list)
     prodd = defaultdict(list)
     spans, items = [], []
+    first = defaultdict(list)  # event -> absolute time of its first occurrence, per CTA
     for cta in tr:
         ev = [(int(t) - t0, int(e)) for t, e in cta[:256] if t]
         pv = [(int(t) - t0, int(e)) for t, e in cta[256:] if t]
@@ -83,6 +89,11 @@ def main():
         spans.append((ev[0][0], ev[-1][0]))
         item_t = [t for t, e in ev if e == 2]
         items.append(len(item_t))
+        seen = set()
+        for t, e in ev + pv:
+            if e not in seen:
+                seen.add(e)
+                first[name(e)].append(t)
         for (ta, ea), (tb, eb) in zip(ev, ev[1:]):
             comp[(name(ea), name(eb))].append(tb - ta)
         for (ta, ea), (tb, eb) in zip(pv, pv[1:]):
@@ -94,6 +105,10 @@ def main():
     print("compute thread 0: mean us between events (count)")
     for k, v in sorted(comp.items(), key=lambda kv: -np.mean(kv[1]) * len(kv[1])):
         print(f"  {k[0]:>14} -> {k[1]:<14} {np.mean(v) / 1e3:8.3f} us  x{len(v)}")
+    print("first occurrence per CTA (us from the earliest entry): min / median / max")
+    for k, v in sorted(first.items(), key=lambda kv: np.median(kv[1])):
+        v = np.array(v) / 1e3
+        print(f"  {k:>14}  {v.min():8.2f} {np.median(v):8.2f} {v.max():8.2f}  x{len(v)}")
     print("producer lane:")
     for k, v in sorted(prodd.items(), key=lambda kv: -np.mean(kv[1]) * len(kv[1])):
         print(f"  {k[0]:>14} -> {k[1]:<14} {np.mean(v) / 1e3:8.3f} us  x{len(v)}")
