@@ -940,6 +940,14 @@ struct Gen {
     std::vector<int> height(nodes.size(), 0);
     for (int n = (int)nodes.size() - 1; n >= 0; --n)
       for (int c : nodes[n].cons) height[n] = std::max(height[n], height[c] + 1);
+    // would scheduling n now force a flush of pending partials?
+    auto would_flush = [&](int n) {
+      const Node& x = nodes[n];
+      bool any = false;
+      for (int k = 0; k < x.nin; ++k) any = any || pending.count(x.in[k]);
+      if (!any || x.kind == SGM_ACCUM) return false;
+      return !(x.kind != SGM_OUTPUT && !d.hints.no_hoist && linear_now(x, pending));
+    };
     auto push_region = [&](auto in_region) {
       std::vector<char> done(nodes.size(), 0);
       for (int n = 0; n < (int)nodes.size(); ++n) done[n] = !in_region(n);
@@ -951,8 +959,12 @@ struct Gen {
           for (int k = 0; k < nodes[n].nin; ++k) ready = ready && (done[nodes[n].in[k]] || !in_region(nodes[n].in[k]));
           // in-region inputs must already be scheduled (done marks both out-of-region and scheduled)
           if (!ready) continue;
-          if (pick < 0 || height[n] > height[pick] ||
-              (height[n] == height[pick] && stream_bytes(nodes[n]) < stream_bytes(nodes[pick])))
+          // nodes that need reduced values wait while anything else is ready, so
+          // one flush (one round of cluster barriers) reduces every partial at once
+          const bool fn = would_flush(n), fp = pick >= 0 && would_flush(pick);
+          if (pick < 0 || (!fn && fp) ||
+              (fn == fp && (height[n] > height[pick] ||
+                            (height[n] == height[pick] && stream_bytes(nodes[n]) < stream_bytes(nodes[pick])))))
             pick = n;
         }
         if (pick < 0) break;
@@ -1716,6 +1728,11 @@ struct Gen {
     os << "  SGM_TR(" << 3000 + 4 * gpos + 2 << ");\n";
   }
 
+  static std::string ew_unroll() {  // experiment knob: unroll factor of elementwise loops
+    const char* u = getenv("SGM_EW_UNROLL");
+    return u ? std::string("#pragma unroll ") + u + "\n" : std::string();
+  }
+
   void emit_node(int n, bool in_loop) {
     Node& x = nodes[n];
     std::string J = in_loop ? "j" : std::to_string(nloop - 1);
@@ -1750,12 +1767,14 @@ struct Gen {
       }
       case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT: case SGM_SCALE: {
         const char* fn = x.kind == SGM_EXP ? "N::ex" : x.kind == SGM_SILU ? "N::silu" : x.kind == SGM_SQUARE ? "N::sq" : "N::sqr";
+        os << ew_unroll();
         os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) " << tile_ptr(n) << "[e] = ";
         if (x.kind == SGM_SCALE) os << "N::scale(" << tile_ptr(x.in[0]) << "[e], (C)" << const_literal(x) << ");\n";
         else os << fn << "(" << tile_ptr(x.in[0]) << "[e]);\n";
         break;
       }
       case SGM_ACCUM: {
+        os << ew_unroll();
         os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) " << tile_ptr(n) << "[e] = N::add("
            << tile_ptr(n) << "[e], " << tile_ptr(x.in[0]) << "[e]);\n";
         break;
@@ -1767,6 +1786,7 @@ struct Gen {
         i64 sa[4], sb[4];
         dense_strides(a.sl, sa);
         dense_strides(b.sl, sb);
+        os << ew_unroll();
         os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) {\n";
         os << "      int r = e; const int i3 = r % " << x.sl[3] << "; r /= " << x.sl[3] << "; const int i2 = r % "
            << x.sl[2] << "; r /= " << x.sl[2] << "; const int i1 = r % " << x.sl[1] << "; const int i0 = r / "
