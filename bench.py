@@ -238,6 +238,8 @@ def main() -> None:
     ap.add_argument("--workloads", default="R,G,A,Q,L")
     ap.add_argument("--budget-us", type=float, default=1000.0, help="(legacy) timing budget per candidate")
     ap.add_argument("--refine-top", type=int, default=3, help="candidates per workload re-timed with 1000 launches")
+    ap.add_argument("--tune-top", type=int, default=8,
+                    help="best sweep candidates per workload whose physical plan variants are tuned (best-kernel phase)")
     ap.add_argument("--best-iters", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -400,11 +402,12 @@ def main() -> None:
     for w in args.workloads:
         wrecs = [r for r in all_recs if r.workload == w]
         ok = sorted((r for r in wrecs if r.error is None and r.latency_us and r.ff_ok is not False),
-                    key=lambda r: (r.latency_us, r.index))[:args.refine_top]
+                    key=lambda r: (r.latency_us, r.index))[:args.tune_top]
         if not ok:
             best[w] = {"error": "no valid candidate"}
             continue
         units_w = {x.index: x for x in P.units(pops[w])}
+        P.precompile_variants([units_w[r.index] for r in ok], ctx[w].numsys)
         tuned = []
         for r in ok:
             lat, hints, plan = P.tune_physical(ctx[w], units_w[r.index], launches=args.best_iters)

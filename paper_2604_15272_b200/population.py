@@ -373,6 +373,22 @@ VARIANT_HINTS = [{}] + [{"variant": v} for v in range(1, 6)] + [{"one_cta": 1}] 
     [{"max_gsplit": g, "max_cluster": 1} for g in (1, 2, 4)] + [{"max_cluster": 1}, {"max_cluster": 2}]
 
 
+def precompile_variants(units: list, numsys: int, threads: int = 0) -> None:
+    """Compile every planner variant of `units` into the cubin cache in parallel
+    (compile-only plans, no device), so tune_physical's plan builds are cache hits."""
+    threads = threads or min(32, os.cpu_count() or 8)
+
+    def one(arg):
+        u, h = arg
+        try:
+            Plan(u.cand, numsys, h or None, None).close()
+        except Exception:
+            pass
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, [(u, h) for u in units for h in VARIANT_HINTS]))
+
+
 def tune_physical(ctx: "WorkloadContext", u: Unit, launches: int = 1000) -> tuple:
     """Physical-plan tuning of one candidate: time each planner variant (other scored
     splits, one-CTA-per-SM rings) over one rotation, re-time the fastest with

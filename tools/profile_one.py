@@ -25,7 +25,9 @@ def main():
     us = P.units(pop)
     if mapping == "best" and isinstance(json.load(open(sys.argv[3])), dict):  # bench --best-out file
         b = json.load(open(sys.argv[3]))[w]
-        u = next(x for x in us if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"])
+        # the same mapping/params can occur under several templates: match the template too
+        u = next(x for x in us if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"]
+                 and pop["candidates"][x.pair]["template_id"] == b.get("template", pop["candidates"][x.pair]["template_id"]))
         variant = b.get("hints") or {}
     elif mapping == "best":
         recs = json.load(open(sys.argv[3]))

@@ -45,7 +45,8 @@ def pick(w, mapping, arg):
     us = P.units(pop)
     if mapping == "best" and isinstance(json.load(open(arg)), dict):  # bench --best-out file
         b = json.load(open(arg))[w]
-        u = next(x for x in us if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"])
+        u = next(x for x in us if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"]
+                 and pop["candidates"][x.pair]["template_id"] == b.get("template", pop["candidates"][x.pair]["template_id"]))
         return pop, u, b.get("hints") or {}
     if mapping == "best":
         recs = [r for r in json.load(open(arg)) if r["workload"] == w and r.get("latency_us") and not r.get("error")]
