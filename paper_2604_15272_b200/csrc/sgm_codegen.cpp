@@ -933,10 +933,7 @@ struct Gen {
           if (all_lin && pending.count(p)) pending.erase(p);
         }
     };
-    // Within each region nodes are list-scheduled by height (longest chain to a sink):
-    // a short dependent chain of small matmuls (LoRA's X@A -> T@B) runs before an
-    // independent big stream (X@W), so its latency hides under the stream, whose boxes
-    // the producer then issues back to back.
+    // Within each region nodes are list-scheduled (see the priority in push_region).
     std::vector<int> height(nodes.size(), 0);
     for (int n = (int)nodes.size() - 1; n >= 0; --n)
       for (int c : nodes[n].cons) height[n] = std::max(height[n], height[c] + 1);
@@ -961,10 +958,20 @@ struct Gen {
           if (!ready) continue;
           // nodes that need reduced values wait while anything else is ready, so
           // one flush (one round of cluster barriers) reduces every partial at once
+          // Among the rest the largest stream goes first: the ring is filled in
+          // schedule order, so a short chain of small matmuls ahead of a big stream
+          // (LoRA's X@A -> T@B before X@W) holds ring slots and delays the big
+          // stream's first boxes, while behind it the chain's few boxes are already
+          // resident when the big stream drains.  Then the longest chain to a sink.
+          // (streamed views emit no code: take them at once so their consumers are ready)
+          const bool vn = nodes[n].kind == SGM_INPUT && nodes[n].store == ST_VIEW;
+          const bool vp = pick >= 0 && nodes[pick].kind == SGM_INPUT && nodes[pick].store == ST_VIEW;
+          if (vp) continue;
+          if (vn) { pick = n; continue; }
           const bool fn = would_flush(n), fp = pick >= 0 && would_flush(pick);
+          const i64 sn = stream_bytes(nodes[n]), sp = pick >= 0 ? stream_bytes(nodes[pick]) : 0;
           if (pick < 0 || (!fn && fp) ||
-              (fn == fp && (height[n] > height[pick] ||
-                            (height[n] == height[pick] && stream_bytes(nodes[n]) < stream_bytes(nodes[pick])))))
+              (fn == fp && (sn > sp || (sn == sp && height[n] > height[pick]))))
             pick = n;
         }
         if (pick < 0) break;
@@ -1920,6 +1927,11 @@ struct Gen {
     } else {
       os << "#define SGM_TR(ev) do {} while (0)\n#define SGM_TRP(ev) do {} while (0)\n";
     }
+    // programmatic dependent launch: the next launch in the stream may start its
+    // CTAs as ours retire; it waits (griddepcontrol.wait) for our completion and
+    // memory before touching global memory.  No-ops without the launch attribute.
+    os << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
+    if (!prod) os << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
     os << "  SGM_TR(0);  // entry\n";
     for (int n = 0; n < (int)nodes.size(); ++n) {
       const Node& x = nodes[n];
@@ -1954,6 +1966,9 @@ struct Gen {
       os << "  }\n";
       os << "  __syncthreads();\n";
       if (CL > 1) os << "  sgm::cluster_sync();\n";
+      // barrier init and descriptor prefetch (kernel parameters only) overlapped the
+      // previous grid's tail; inputs, outputs and scratch wait for its completion
+      os << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
       os << "  if (tid >= NT) {\n";
       emit_producer();
       os << "  }\n";

@@ -85,6 +85,7 @@ struct Driver {
   SGM_FN(cuFuncGetAttribute, int*, CUfunction_attribute, CUfunction)
   SGM_FN(cuLaunchKernel, CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
          void**, void**)
+  SGM_FN(cuLaunchKernelEx, const CUlaunchConfig*, CUfunction, void**, void**)
   SGM_FN(cuMemAlloc, CUdeviceptr*, size_t)
   SGM_FN(cuMemFree, CUdeviceptr)
   SGM_FN(cuMemHostAlloc, void**, size_t, unsigned)
@@ -140,6 +141,7 @@ struct Driver {
     g &= sym(cuFuncSetAttribute, "cuFuncSetAttribute");
     g &= sym(cuFuncGetAttribute, "cuFuncGetAttribute");
     g &= sym(cuLaunchKernel, "cuLaunchKernel");
+    sym(cuLaunchKernelEx, "cuLaunchKernelEx");  // optional: programmatic dependent launch
     g &= sym(cuMemAlloc, "cuMemAlloc_v2");
     g &= sym(cuMemFree, "cuMemFree_v2");
     g &= sym(cuMemHostAlloc, "cuMemHostAlloc");
@@ -616,8 +618,30 @@ static int launch_plan(sgm_plan* p, const void* const* inputs, void* const* outp
   for (int k = 0; k < p->n_out; ++k) args.out[k] = outputs[k];
   args.scratch = (void*)p->scratch;
   void* params[] = {&args};
-  CU(D.cuLaunchKernel(p->fn, (unsigned)p->launch_ctas, 1, 1, (unsigned)p->gen.threads, 1, 1,
-                      (unsigned)p->gen.smem_bytes, s, params, nullptr));
+  static const bool pdl = getenv("SGM_NO_PDL") == nullptr;
+  if (pdl && D.cuLaunchKernelEx) {
+    // programmatic stream serialization: this grid may launch while the previous
+    // kernel in the stream drains; the generated code's griddepcontrol.wait keeps
+    // every global access after that kernel's completion
+    CUlaunchAttribute attr;
+    memset(&attr, 0, sizeof attr);
+    attr.id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr.value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDimX = (unsigned)p->launch_ctas;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = (unsigned)p->gen.threads;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)p->gen.smem_bytes;
+    cfg.hStream = s;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    CU(D.cuLaunchKernelEx(&cfg, p->fn, params, nullptr));
+  } else {
+    CU(D.cuLaunchKernel(p->fn, (unsigned)p->launch_ctas, 1, 1, (unsigned)p->gen.threads, 1, 1,
+                        (unsigned)p->gen.smem_bytes, s, params, nullptr));
+  }
   g_launches++;  // during graph capture this counts the captured node once
   return SGM_OK;
 }
