@@ -958,20 +958,19 @@ struct Gen {
           if (!ready) continue;
           // nodes that need reduced values wait while anything else is ready, so
           // one flush (one round of cluster barriers) reduces every partial at once
-          // Among the rest the largest stream goes first: the ring is filled in
-          // schedule order, so a short chain of small matmuls ahead of a big stream
-          // (LoRA's X@A -> T@B before X@W) holds ring slots and delays the big
-          // stream's first boxes, while behind it the chain's few boxes are already
-          // resident when the big stream drains.  Then the longest chain to a sink.
           // (streamed views emit no code: take them at once so their consumers are ready)
           const bool vn = nodes[n].kind == SGM_INPUT && nodes[n].store == ST_VIEW;
           const bool vp = pick >= 0 && nodes[pick].kind == SGM_INPUT && nodes[pick].store == ST_VIEW;
           if (vp) continue;
           if (vn) { pick = n; continue; }
+          // Then the longest chain to a sink: a short chain of small matmuls (LoRA's
+          // X@A -> T@B) runs before an independent big stream (X@W) while the ring
+          // pre-fills with the big stream's boxes (measured: W first is ~5% slower
+          // on L).  Ties: the smaller stream first.
           const bool fn = would_flush(n), fp = pick >= 0 && would_flush(pick);
           const i64 sn = stream_bytes(nodes[n]), sp = pick >= 0 ? stream_bytes(nodes[pick]) : 0;
           if (pick < 0 || (!fn && fp) ||
-              (fn == fp && (sn > sp || (sn == sp && height[n] > height[pick]))))
+              (fn == fp && (height[n] > height[pick] || (height[n] == height[pick] && sn < sp))))
             pick = n;
         }
         if (pick < 0) break;
@@ -1454,7 +1453,9 @@ struct Gen {
   // Measured on B200 (tools/bench_tma_ring.cu): TMA streaming reaches ~6.3 TB/s with
   // 32 KB stages at one CTA per SM, or 16 KB stages at two CTAs per SM; 8 KB
   // stages stall near 3.8 TB/s whatever the ring depth.
+  bool paired = false;  // the ring plan counts on two CTAs per SM
   void plan_ring() {
+    paired = false;
     if (!prod) { ringS = 0; return; }
     int base = (smem_peak + 1023) / 1024 * 1024;
     const int stg = (int)stage_total;
@@ -1463,7 +1464,7 @@ struct Gen {
     int S = std::min(6, (kSmemCap - base - 1024 - stg) / slotB);
     if (ctas > num_sms && !uses_tc() && !d.hints.one_cta) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM (no TMEM users)
       int S2 = (110 * 1024 - base - 1024 - stg) / 16384;
-      if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); }
+      if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); paired = true; }
     }
     if (S < 3) { slotB = 16384; S = std::min(12, (kSmemCap - base - 1024 - stg) / slotB); }
     for (auto& x : nodes) {
@@ -1710,13 +1711,13 @@ struct Gen {
   void emit_gflush(const std::vector<int>& fl, int gpos) {
     i64 fo[SGM_MAX_NODES];
     i64 tot = 0;
-    for (int f : fl) { fo[f] = tot; tot += prod4(nodes[f].sl); }
+    for (int f : fl) { fo[f] = tot; tot += (prod4(nodes[f].sl) + 3) / 4 * 4; }  // 16-byte aligned slots
     gws_tile = tot;
     os << "    {\n      C* gw = (C*)((unsigned char*)a.scratch + " << gws_off << "LL);\n";
     os << "      unsigned* gcnt = (unsigned*)((unsigned char*)a.scratch + " << gcnt_off << "LL);\n";
     for (int f : fl)
-      os << "      for (int e = tid; e < " << prod4(nodes[f].sl) << "; e += NT) gw[(grp * " << GP << " + gpart) * "
-         << tot << "LL + " << fo[f] << " + e] = " << tile_ptr(f) << "[e];\n";
+      os << "      sgm::gws_store<N, " << prod4(nodes[f].sl) << ", NT>(gw + (grp * " << GP << " + gpart) * " << tot
+         << "LL + " << fo[f] << ", " << tile_ptr(f) << ");\n";
     // the CTA barrier orders every thread's partial stores before thread 0's
     // acq_rel counter update (cumulativity), so one gpu-scope RMW replaces a
     // fence per thread; the last arrival's acquire covers all groups' partials
@@ -1727,17 +1728,23 @@ struct Gen {
     os << "  if (sgm_last) {\n";
     os << "    {\n      const C* gw = (const C*)((unsigned char*)a.scratch + " << gws_off << "LL);\n";
     for (int f : fl)
-      os << "      for (int e = tid; e < " << prod4(nodes[f].sl) << "; e += NT) { A acc = N::azero(); for (int q = 0; q < "
-         << GP << "; ++q) N::aadd(acc, __ldcg(&gw[(grp * " << GP << " + q) * " << tot << "LL + " << fo[f]
-         << " + e])); " << tile_ptr(f) << "[e] = N::fin(acc); }\n";
+      os << "      sgm::gws_reduce<N, " << prod4(nodes[f].sl) << ", " << GP << ", " << tot << "LL, NT>(" << tile_ptr(f)
+         << ", gw + grp * " << GP * tot << "LL + " << fo[f] << ");\n";
     os << "      if (tid == 0) ((unsigned*)((unsigned char*)a.scratch + " << gcnt_off << "LL))[grp] = 0u;\n";
     os << "      sgm::csync<NT>();\n    }\n";
     os << "  SGM_TR(" << 3000 + 4 * gpos + 2 << ");\n";
   }
 
-  static std::string ew_unroll() {  // experiment knob: unroll factor of elementwise loops
-    const char* u = getenv("SGM_EW_UNROLL");
-    return u ? std::string("#pragma unroll ") + u + "\n" : std::string();
+  // Elementwise map over node n's tile: each thread computes 4 elements into
+  // registers before storing any.  In-place ops (output aliasing an operand)
+  // otherwise serialise every iteration's loads behind the previous store.
+  void emit_map(int n, const std::string& pre, const std::string& expr) {
+    const i64 sz = prod4(nodes[n].sl);
+    os << "    for (int e0 = tid; e0 < " << sz << "; e0 += 4 * NT) {\n      C v_[4];\n";
+    os << "#pragma unroll\n      for (int j = 0; j < 4; ++j) {\n        const int e = e0 + j * NT;\n";
+    os << "        if (e < " << sz << ") { " << pre << "v_[j] = " << expr << "; }\n      }\n";
+    os << "#pragma unroll\n      for (int j = 0; j < 4; ++j) {\n        const int e = e0 + j * NT;\n";
+    os << "        if (e < " << sz << ") " << tile_ptr(n) << "[e] = v_[j];\n      }\n    }\n";
   }
 
   void emit_node(int n, bool in_loop) {
@@ -1774,16 +1781,14 @@ struct Gen {
       }
       case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT: case SGM_SCALE: {
         const char* fn = x.kind == SGM_EXP ? "N::ex" : x.kind == SGM_SILU ? "N::silu" : x.kind == SGM_SQUARE ? "N::sq" : "N::sqr";
-        os << ew_unroll();
-        os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) " << tile_ptr(n) << "[e] = ";
-        if (x.kind == SGM_SCALE) os << "N::scale(" << tile_ptr(x.in[0]) << "[e], (C)" << const_literal(x) << ");\n";
-        else os << fn << "(" << tile_ptr(x.in[0]) << "[e]);\n";
+        std::ostringstream ex;
+        if (x.kind == SGM_SCALE) ex << "N::scale(" << tile_ptr(x.in[0]) << "[e], (C)" << const_literal(x) << ")";
+        else ex << fn << "(" << tile_ptr(x.in[0]) << "[e])";
+        emit_map(n, "", ex.str());
         break;
       }
       case SGM_ACCUM: {
-        os << ew_unroll();
-        os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) " << tile_ptr(n) << "[e] = N::add("
-           << tile_ptr(n) << "[e], " << tile_ptr(x.in[0]) << "[e]);\n";
+        emit_map(n, "", "N::add(" + tile_ptr(n) + "[e], " + tile_ptr(x.in[0]) + "[e])");
         break;
       }
       case SGM_DIV: case SGM_MUL: case SGM_ADD: {
@@ -1793,11 +1798,10 @@ struct Gen {
         i64 sa[4], sb[4];
         dense_strides(a.sl, sa);
         dense_strides(b.sl, sb);
-        os << ew_unroll();
-        os << "    for (int e = tid; e < " << prod4(x.sl) << "; e += NT) {\n";
-        os << "      int r = e; const int i3 = r % " << x.sl[3] << "; r /= " << x.sl[3] << "; const int i2 = r % "
-           << x.sl[2] << "; r /= " << x.sl[2] << "; const int i1 = r % " << x.sl[1] << "; const int i0 = r / "
-           << x.sl[1] << ";\n";
+        std::ostringstream pre;
+        pre << "int r = e; const int i3 = r % " << x.sl[3] << "; r /= " << x.sl[3] << "; const int i2 = r % " << x.sl[2]
+            << "; r /= " << x.sl[2] << "; const int i1 = r % " << x.sl[1] << "; const int i0 = r / " << x.sl[1]
+            << "; (void)i0; (void)i1; (void)i2; (void)i3; ";
         auto idx = [&](const i64* s, const i64* sl) {
           std::ostringstream q;
           q << "0";
@@ -1806,8 +1810,10 @@ struct Gen {
             if (sl[k] > 1) q << " + " << iv[k] << " * " << s[k];
           return q.str();
         };
-        os << "      " << tile_ptr(n) << "[e] = " << fn << "(" << tile_ptr(x.in[0]) << "[" << idx(sa, a.sl) << "], "
-           << tile_ptr(x.in[1]) << "[" << idx(sb, b.sl) << "]);\n    }\n";
+        std::ostringstream ex;
+        ex << fn << "(" << tile_ptr(x.in[0]) << "[" << idx(sa, a.sl) << "], " << tile_ptr(x.in[1]) << "["
+           << idx(sb, b.sl) << "])";
+        emit_map(n, pre.str(), ex.str());
         break;
       }
       case SGM_SUM: {
@@ -1897,7 +1903,9 @@ struct Gen {
        << ", loop parts " << LP << "\n";
     os << "typedef " << nstruct() << " N;\ntypedef N::S S;\ntypedef N::C C;\ntypedef N::A A;\n";
     os << "#define NT " << NT << "\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(" << (prod ? NT + 32 : NT) << ")";
+    // a paired plan must get its two CTAs per SM: cap registers at 64K / (2 x threads)
+    // (the fp32 consumer otherwise compiled to ~116 and ran one CTA per SM at 3x the time)
+    os << "extern \"C\" __global__ void __launch_bounds__(" << (prod ? NT + 32 : NT) << (paired ? ", 2" : "") << ")";
     if (CL > 1) os << " __cluster_dims__(" << CL << ", 1, 1)";
     os << " @KNAME@(const __grid_constant__ sgm::Args a) {\n";
     os << "  extern __shared__ __align__(1024) unsigned char sm[];\n";
@@ -2081,7 +2089,7 @@ struct Gen {
       i64 gt = 0;
       for (auto& e : sched)
         if (e.type == Ev::GFLUSH)
-          for (int f : e.flush) gt += prod4(nodes[f].sl);
+          for (int f : e.flush) gt += (prod4(nodes[f].sl) + 3) / 4 * 4;  // 16-byte aligned slots
       const i64 work_ctas = LB * FP * GP * CL;
       gws_off = (work_ctas * scratch_per_cta + 255) / 256 * 256;
       gcnt_off = gws_off + (LB * FP * GP * gt * ec + 255) / 256 * 256;

@@ -1077,6 +1077,50 @@ __device__ __forceinline__ void stage_convert(typename N::C* __restrict__ dst, c
 // Cluster barrier among compute threads only (the producer warp may be blocked
 // on its ring and must not be counted): thread 0 of every CTA arrives on every
 // peer's `bar` (count CL) with release.cluster and waits with acquire.cluster.
+// gsplit workspace traffic in 16-byte vectors (slots are 16-byte aligned).
+// gws_store: one part's partial tile -> its slot.  gws_reduce: the group's
+// last item sums the GP slots in part order (fixed order: bit-identical
+// results whatever the arrival order); GP independent 16-byte loads per
+// thread are in flight at once instead of one scalar chain per element.
+template <class N, int SZ, int NT>
+__device__ __forceinline__ void gws_store(typename N::C* __restrict__ gw, const typename N::C* __restrict__ t) {
+  typedef typename N::C C;
+  constexpr int VW = 16 / sizeof(C);
+  constexpr int NV = SZ / VW;
+  for (int v = threadIdx.x; v < NV; v += NT) {
+    union { uint4 q; C c[VW]; } u;
+#pragma unroll
+    for (int i = 0; i < VW; ++i) u.c[i] = t[v * VW + i];
+    __stcg(reinterpret_cast<uint4*>(gw) + v, u.q);
+  }
+  for (int e = NV * VW + threadIdx.x; e < SZ; e += NT) gw[e] = t[e];
+}
+
+template <class N, int SZ, int GP, i64 STRIDE, int NT>
+__device__ __forceinline__ void gws_reduce(typename N::C* __restrict__ t, const typename N::C* __restrict__ gw) {
+  typedef typename N::C C;
+  typedef typename N::A Acc;
+  constexpr int VW = 16 / sizeof(C);
+  constexpr int NV = SZ / VW;
+  for (int v = threadIdx.x; v < NV; v += NT) {
+    union U { uint4 q; C c[VW]; } u[GP];
+#pragma unroll
+    for (int q = 0; q < GP; ++q) u[q].q = __ldcg(reinterpret_cast<const uint4*>(gw + q * STRIDE) + v);
+#pragma unroll
+    for (int i = 0; i < VW; ++i) {
+      Acc acc = N::azero();
+#pragma unroll
+      for (int q = 0; q < GP; ++q) N::aadd(acc, u[q].c[i]);
+      t[v * VW + i] = N::fin(acc);
+    }
+  }
+  for (int e = NV * VW + threadIdx.x; e < SZ; e += NT) {
+    Acc acc = N::azero();
+    for (int q = 0; q < GP; ++q) N::aadd(acc, __ldcg(&gw[q * STRIDE + e]));
+    t[e] = N::fin(acc);
+  }
+}
+
 // Cluster barrier on one mbarrier per CTA (count CL): lanes 0..CL-1 each signal
 // one peer with a release arrive (in parallel: one lane issuing CL dependent
 // release arrives measured ~1.5 us per barrier, this ~0.9 us), thread 0 polls
