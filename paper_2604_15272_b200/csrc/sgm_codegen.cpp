@@ -608,7 +608,8 @@ struct Gen {
     // residency: two CTAs per SM when the tiles leave room for a 3 x 16 KB ring in half an SM
     // measured: the occupancy of kernels that use tcgen05 (TMEM) is one CTA per SM
     // whatever their shared memory, so only CUDA-core kernels can pair up
-    const bool two = prod && !uses_tc() && !d.hints.one_cta && peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
+    const bool two = prod && (!uses_tc() || tc_pairable()) && !d.hints.one_cta &&
+                     peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
     const int cps = two ? 2 : 1;
     const i64 items = LB * FP * GP;
     const i64 slots = std::max<i64>(1, resident_ctas(CL, num_sms) * cps / CL);
@@ -824,6 +825,19 @@ struct Gen {
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) return true;
     return false;
+  }
+  // Two TMEM-using CTAs share an SM when each allocates at most half of TMEM
+  // (256 columns): measured on B200 (tools/tmem_occ_probe.cu) the hardware
+  // co-schedules them although the occupancy API reports one CTA per SM.
+  // Streamed tiles (ntl <= 16) fit with fewer accumulators; the cp.async GEMV
+  // path needs ntl * 16 columns.
+  bool tc_pairable() const {
+    for (auto& x : nodes) {
+      if (!(x.kind == SGM_MATMUL && x.gemv && x.tc)) continue;
+      const i64 ntl = (x.sl[3] + 127) / 128;
+      if (ntl * 16 > 256) return false;
+    }
+    return true;
   }
 
   // pending partials + schedule
@@ -1462,7 +1476,7 @@ struct Gen {
     i64 ctas = LB * FP * GP * CL;
     slotB = 32768;
     int S = std::min(6, (kSmemCap - base - 1024 - stg) / slotB);
-    if (ctas > num_sms && !uses_tc() && !d.hints.one_cta) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM (no TMEM users)
+    if (ctas > num_sms && (!uses_tc() || tc_pairable()) && !d.hints.one_cta) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM
       int S2 = (110 * 1024 - base - 1024 - stg) / 16384;
       if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); paired = true; }
     }
@@ -1472,6 +1486,16 @@ struct Gen {
       if (x.tc) while (x.kc * 256 > slotB) x.kc /= 2;
       else while (x.kc * x.bw * 4 > slotB) x.kc /= 2;
     }
+    if (paired)  // half of TMEM per CTA: fewer independent accumulators
+      for (auto& x : nodes) {
+        if (!(x.kind == SGM_MATMUL && x.gemv && x.tc)) continue;
+        const i64 ntl = (x.sl[3] + 127) / 128;
+        if (x.tma)
+          while (x.acc > 1 && ntl * x.acc * 16 > 256) x.acc /= 2;
+        int cols = 32;
+        while (cols < ntl * (x.tma ? x.acc : 1) * 16) cols *= 2;
+        x.tc_cols = cols;
+      }
     ringS = S;
     ring_off = base;
     smem_peak = base + 1024 + S * slotB + stg;
@@ -1741,8 +1765,11 @@ struct Gen {
   void emit_map(int n, const std::string& pre, const std::string& expr) {
     const i64 sz = prod4(nodes[n].sl);
     os << "    for (int e0 = tid; e0 < " << sz << "; e0 += 4 * NT) {\n      C v_[4];\n";
-    os << "#pragma unroll\n      for (int j = 0; j < 4; ++j) {\n        const int e = e0 + j * NT;\n";
-    os << "        if (e < " << sz << ") { " << pre << "v_[j] = " << expr << "; }\n      }\n";
+    // compute with the index clamped (no branch around the loads, so the four are
+    // issued back to back); only the stores are guarded
+    os << "#pragma unroll\n      for (int j = 0; j < 4; ++j) {\n        const int e = min(e0 + j * NT, " << sz - 1
+       << ");\n";
+    os << "        { " << pre << "v_[j] = " << expr << "; }\n      }\n";
     os << "#pragma unroll\n      for (int j = 0; j < 4; ++j) {\n        const int e = e0 + j * NT;\n";
     os << "        if (e < " << sz << ") " << tile_ptr(n) << "[e] = v_[j];\n      }\n    }\n";
   }
@@ -2118,6 +2145,7 @@ struct Gen {
     R.ctas = LB * FP * GP * CL;
     R.threads = prod ? NT + 32 : NT;
     R.ring_slots = ringS;
+    R.ctas_per_sm = paired ? 2 : 1;
     std::vector<TmaSpec> specs(4);
     int nspec = 0;
     for (auto& x : nodes) {

@@ -37,6 +37,7 @@ struct GenResult {
   int n_tcgen05 = 0;
   int n_tma = 0;               // streamed matmuls fed by the TMA producer warp
   int ring_slots = 0;
+  int ctas_per_sm = 1;         // the plan counts on this many co-resident CTAs per SM
   std::vector<TmaSpec> tmaps;
   std::string summary;
 };

@@ -10,7 +10,7 @@
 //
 // Semantics follow the reference interpreter (pkg/src/symfuse/interp.py):
 //   apply_op (interp.py:45-66)   -> unary/binary/sum/matmul/scale below
-//   _silu    (interp.py:36-42)   -> NF64::silu / NF32::silu (same two branches)
+//   _silu    (interp.py:36-42)   -> NF64::silu (same two branches) / NF32::silu (branch-free, same function)
 //   accum    (interp.py:171-176) -> plain sums (order-insensitive up to fp rounding)
 // and the finite-field restatement in oracle/ff_np.py (bit-exact).
 #pragma once
@@ -117,11 +117,19 @@ struct NF32 {
   __device__ static __forceinline__ C nan() { return __int_as_float(0x7fc00000); }
   __device__ static __forceinline__ C add(C a, C b) { return a + b; }
   __device__ static __forceinline__ C mul(C a, C b) { return a * b; }
-  // correctly rounded reciprocal + one residual correction: the IEEE quotient in
-  // all but extreme-exponent cases, without the divergent slow-path call of '/'
-  // (which the 0-, inf- and NaN-producing cases below fall back to exactly)
+  // Branch-free quotient: approximate reciprocal, one Newton step, one residual
+  // correction (the IEEE quotient in all but extreme-exponent cases).  '/' and
+  // __frcp_rn carry a slow-path call whose branch keeps the compiler from
+  // overlapping consecutive elements.  0, inf and NaN cases fall back by select
+  // to the plain product (a/0 = inf, a/inf = 0, 0/0 = NaN as in IEEE).
+  __device__ static __forceinline__ C rcp(C b) {
+    C r;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(b));
+    const C r2 = r * fmaf(-b, r, 2.0f);
+    return isfinite(r2) ? r2 : r;
+  }
   __device__ static __forceinline__ C div(C a, C b) {
-    const C r = __frcp_rn(b);
+    const C r = rcp(b);
     const C q = a * r;
     const C q2 = fmaf(r, fmaf(-b, q, a), q);
     return isfinite(q2) ? q2 : q;
@@ -133,7 +141,7 @@ struct NF32 {
   // (~2 ulp overall) instead of a divergent IEEE division with its slow path
   __device__ static __forceinline__ C silu(C x) {
     const C e = expf(-fabsf(x));
-    const C r = __frcp_rn(1.0f + e);
+    const C r = rcp(1.0f + e);  // 1 + e in [1, 2]: no special cases
     return x * (x >= 0.0f ? r : e * r);
   }
   __device__ static __forceinline__ C scale(C x, C c) { return c * x; }

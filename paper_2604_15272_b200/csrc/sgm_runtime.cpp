@@ -480,6 +480,13 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
       if (D.cuOccupancyMaxActiveBlocksPerMultiprocessor(&nb, p->fn, gr.threads, (size_t)gr.smem_bytes) == CUDA_SUCCESS &&
           nb > 0)
         resident = (int64_t)nb * g_dev[t_device].sms;
+      // the occupancy API counts a TMEM-allocating kernel as one CTA per SM, but the
+      // hardware co-schedules two that each take at most half of TMEM (the planner
+      // pairs only those): trust the plan there
+      if (gr.ctas_per_sm > nb && gr.n_tcgen05 > 0 && gr.smem_bytes <= 113 * 1024) {
+        nb = gr.ctas_per_sm;
+        resident = (int64_t)nb * g_dev[t_device].sms;
+      }
       p->occ_per_sm = nb;
       if (getenv("SGM_OCC_DEBUG"))
         for (int kb : {16, 32, 48, 64, 80, 90, 96, 100, 104, 108, 112}) {

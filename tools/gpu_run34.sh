@@ -1,0 +1,10 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o /tmp/tmem_occ tools/tmem_occ_probe.cu && timeout 60 /tmp/tmem_occ
+for W in L A Q; do echo "== $W paired default"; timeout 300 python tools/trace_one.py $W best tools/data/best_r32.json 2>&1 | head -16 | cut -c1-200; done
+timeout 1200 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -4 gpurun_out/pytest_gpu.log
+timeout 1500 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --records gpurun_out/records.json --best-out gpurun_out/best.json > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc $?"
+tail -3 gpurun_out/bench.err
+python -c "
+import json; b=json.load(open('gpurun_out/best.json'))
+for w,x in b.items(): print(w, '%.2f us'%x['latency_us'], '%.0f%%'%(100*x['frac_hbm']), x['template'], x['hints'], x['params'], x['mapping'], x['plan'][:150])
+"
