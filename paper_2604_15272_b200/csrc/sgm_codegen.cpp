@@ -67,7 +67,10 @@ uint32_t ff_const(int64_t num, int64_t den) {
 
 namespace {
 
-enum Store { ST_NONE = 0, ST_VIEW, ST_SMEM, ST_GLOBAL };
+// ST_XG: a bf16 input used only as the A operand of streamed tcgen05 matmuls; no
+// tile, its A^T buffer is built straight from global memory (bf16 is exact: no
+// fp32 staging tile, no residual rows)
+enum Store { ST_NONE = 0, ST_VIEW, ST_SMEM, ST_GLOBAL, ST_XG };
 
 struct Node {
   int kind = 0, nin = 0, in[2] = {-1, -1}, slot = -1, axis = -1;
@@ -1039,6 +1042,8 @@ struct Gen {
   // matmul realisation choices (depend on slices)
   void matmul_choices() {
     int ntma = 0;
+    for (auto& t : nodes)
+      if (t.store == ST_XG) t.store = ST_SMEM;
     for (int n = 0; n < (int)nodes.size(); ++n) {
       Node& x = nodes[n];
       if (x.kind != SGM_MATMUL) continue;
@@ -1150,6 +1155,17 @@ struct Gen {
         }
       }
     }
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& t = nodes[n];
+      if (t.kind != SGM_INPUT || t.store != ST_SMEM || t.body || t.cons.empty() || ns != SGM_BF16) continue;
+      const i64* st = in_strides[t.slot];
+      bool ok = st[3] == 1 && (st[2] * 2) % 16 == 0 && t.sl[3] % 8 == 0 && t.sl[2] <= 16 && t.sl[0] * t.sl[1] == 1;
+      for (int c : t.cons) {
+        const Node& m = nodes[c];
+        ok = ok && m.kind == SGM_MATMUL && m.tma && m.tc && m.xb_shared && m.in[0] == n && m.in[1] != n;
+      }
+      if (ok && !d.hints.no_tma) t.store = ST_XG;
+    }
     prod = false;
     int id = 0;
     for (auto& x : nodes)
@@ -1218,7 +1234,7 @@ struct Gen {
       x.inv = false;
       if (d.hints.no_hoist || LB * FP * GP <= 1) continue;
       if (x.body || x.pend || x.gpend || x.kind == SGM_OUTPUT || x.kind == SGM_ACCUM) continue;
-      if (x.store != ST_SMEM && x.store != ST_GLOBAL) continue;
+      if (x.store != ST_SMEM && x.store != ST_GLOBAL && x.store != ST_XG) continue;
       if (free_split(x)) continue;
       if (x.kind == SGM_INPUT) {
         bool dep = false;
@@ -1781,7 +1797,7 @@ struct Gen {
        << x.sl[3] << "]\n";
     switch (x.kind) {
       case SGM_INPUT: {
-        if (x.store == ST_VIEW) return;  // streamed by its consumer (pointer built there)
+        if (x.store == ST_VIEW || x.store == ST_XG) return;  // read by its consumer (pointer built there)
         if (x.staged) {
           os << "    sgm::mbar_wait(&sfull[" << x.stage_id << "], cit & 1u);\n";
           os << "    sgm::stage_convert<N, " << x.sl[0] << ", " << x.sl[1] << ", " << x.sl[2] << ", " << x.sl[3] << ", "
@@ -1870,10 +1886,20 @@ struct Gen {
         };
         std::string pa = a.store == ST_VIEW ? view_ptr(a) : tile_ptr(x.in[0]);
         std::string pb = b.store == ST_VIEW ? view_ptr(b) : tile_ptr(x.in[1]);
+        bool build = x.xb_build;
+        if (x.tma && x.tc && a.store == ST_XG) {
+          if (x.xb_build) {
+            os << "    sgm::build_xb_g<" << M << ", " << K << ", " << in_strides[a.slot][2] << "LL, NT>((u16*)(sm + "
+               << x.at_off << "), (const u16*)" << view_ptr(a) << ");\n";
+            os << "    sgm::fence_async_smem();\n    sgm::csync<NT>();\n";
+          }
+          pa = "(const float*)nullptr";
+          build = false;
+        }
         if (x.tma && x.tc) {
           os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS << ", "
-             << slotB << ", NT, " << (x.xb_build ? "true" : "false") << ", " << x.acc << ">(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
+             << slotB << ", NT, " << (build ? "true" : "false") << ", " << x.acc << ">(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
              << ", tmem_base, ring, full, empty, done, sq, sdph);\n";
         } else if (x.tma) {
           os << "    sgm::mm_stream_f32<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
@@ -2037,8 +2063,13 @@ struct Gen {
         if (!first) continue;
         i64 sa[4];
         dense_strides(a.sl, sa);
-        os << "  sgm::build_xb<" << x.sl[2] << ", " << a.sl[3] << ", " << sa[2] << "LL, " << sa[3] << "LL, NT>((u16*)(sm + "
-           << x.at_off << "), " << tile_ptr(x.in[0]) << ");\n";
+        if (a.store == ST_XG)
+          os << "  sgm::build_xb_g<" << x.sl[2] << ", " << a.sl[3] << ", " << in_strides[a.slot][2]
+             << "LL, NT>((u16*)(sm + " << x.at_off << "), (const u16*)((const S*)a.in[" << a.slot << "] + ("
+             << offset_expr(a, true, std::to_string(nloop - 1)) << ")));\n";
+        else
+          os << "  sgm::build_xb<" << x.sl[2] << ", " << a.sl[3] << ", " << sa[2] << "LL, " << sa[3]
+             << "LL, NT>((u16*)(sm + " << x.at_off << "), " << tile_ptr(x.in[0]) << ");\n";
         os << "  sgm::fence_async_smem();\n  sgm::csync<NT>();\n";
       }
     }

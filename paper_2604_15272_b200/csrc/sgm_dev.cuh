@@ -868,6 +868,34 @@ __device__ __forceinline__ void build_xb(u16* __restrict__ xb, const float* __re
   }
 }
 
+// A^T straight from a bf16 global row-major A[M][K] (row stride SA2, unit K
+// stride): chunk (k8, m) is the 16 bytes at A[m][k8*8..].  bf16 is exact, so
+// rows M.. (padding, and the residual rows when M <= 8) are zero.  Lane order
+// m-fastest makes each store phase one contiguous 128-byte core matrix; the
+// loads (up to 8 in flight per thread) mostly hit L2, A being shared by CTAs.
+template <int M, int K, i64 SA2, int NT>
+__device__ __forceinline__ void build_xb_g(u16* __restrict__ xb, const u16* __restrict__ A) {
+  static_assert(K % 8 == 0 && M <= 16, "build_xb_g shape");
+  constexpr int TOT = 2 * K;  // (k8, m) chunks, m in 0..15
+  constexpr int IT = (TOT + NT - 1) / NT;
+  constexpr int BT = IT < 8 ? IT : 8;
+  for (int b = 0; b < IT; b += BT) {
+    uint4 v[BT];
+#pragma unroll
+    for (int j = 0; j < BT; ++j) {
+      const int c = threadIdx.x + (b + j) * NT;
+      const int m = c & 15, k8 = c >> 4;
+      v[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (b + j < IT && c < TOT && m < M) v[j] = __ldg(reinterpret_cast<const uint4*>(A + (i64)m * SA2 + k8 * 8));
+    }
+#pragma unroll
+    for (int j = 0; j < BT; ++j) {
+      const int c = threadIdx.x + (b + j) * NT;
+      if (b + j < IT && c < TOT) *reinterpret_cast<uint4*>(xb + (i64)c * 8) = v[j];
+    }
+  }
+}
+
 // BUILD = false: the caller already built xbuf (shared A operand, or an
 // item-invariant one built once per CTA); requires B0 * B1 == 1.
 // ACC independent accumulators per tile (TMEM columns (t*ACC + a)*16): MMAs into
