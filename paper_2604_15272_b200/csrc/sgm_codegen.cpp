@@ -611,8 +611,7 @@ struct Gen {
     // residency: two CTAs per SM when the tiles leave room for a 3 x 16 KB ring in half an SM
     // measured: the occupancy of kernels that use tcgen05 (TMEM) is one CTA per SM
     // whatever their shared memory, so only CUDA-core kernels can pair up
-    const bool two = prod && (!uses_tc() || tc_pairable()) && !d.hints.one_cta &&
-                     peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
+    const bool two = prod && pairable() && !d.hints.one_cta && peak + 3 * 16384 + 1024 + stage_total <= 110 * 1024;
     const int cps = two ? 2 : 1;
     const i64 items = LB * FP * GP;
     const i64 slots = std::max<i64>(1, resident_ctas(CL, num_sms) * cps / CL);
@@ -834,6 +833,12 @@ struct Gen {
   // co-schedules them although the occupancy API reports one CTA per SM.
   // Streamed tiles (ntl <= 16) fit with fewer accumulators; the cp.async GEMV
   // path needs ntl * 16 columns.
+  // Which producer kernels pair up.  Measured on a plain fp32 GEMV (64 MB,
+  // tools/gemv_probe.py): paired 23.8 us vs one CTA per SM 16.8 us -- the
+  // CUDA-core fp32 consumer (2 FMA per streamed byte) does not gain from a
+  // second CTA and loses registers to the 2-CTA launch bound; the tcgen05
+  // kernels gain (G 73% -> 82% of the roofline).
+  bool pairable() const { return uses_tc() && tc_pairable(); }
   bool tc_pairable() const {
     for (auto& x : nodes) {
       if (!(x.kind == SGM_MATMUL && x.gemv && x.tc)) continue;
@@ -1357,15 +1362,23 @@ struct Gen {
         at_iv[n] = I.id;
       }
     for (int p = 0; p < S; ++p)
-      if (sched[p].type == Ev::FLUSH)
+      if (sched[p].type == Ev::FLUSH) {
+        const bool push = push_flush(sched[p].flush);
         for (int f : sched[p].flush) {
           Interval I;
           I.id = -(1 + tcount++);
-          I.start = I.end = p;
-          I.bytes = prod4(nodes[f].sl) * ec;
+          if (push) {  // receive buffers: written by peers at any time, live for the whole kernel
+            I.start = 0;
+            I.end = S;
+            I.bytes = 2 * CL * pad4(prod4(nodes[f].sl)) * ec;
+          } else {
+            I.start = I.end = p;
+            I.bytes = prod4(nodes[f].sl) * ec;
+          }
           iv.push_back(I);
           flush_ids.push_back({{p, f}, I.id});
         }
+      }
     std::sort(iv.begin(), iv.end(), [](const Interval& a, const Interval& b) {
       if (a.start != b.start) return a.start < b.start;
       return a.bytes > b.bytes;
@@ -1492,7 +1505,7 @@ struct Gen {
     i64 ctas = LB * FP * GP * CL;
     slotB = 32768;
     int S = std::min(6, (kSmemCap - base - 1024 - stg) / slotB);
-    if (ctas > num_sms && (!uses_tc() || tc_pairable()) && !d.hints.one_cta) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM
+    if (ctas > num_sms && pairable() && !d.hints.one_cta) {  // two CTAs per SM if 3+ 16 KB slots fit in half the SM
       int S2 = (110 * 1024 - base - 1024 - stg) / 16384;
       if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); paired = true; }
     }
@@ -1721,7 +1734,40 @@ struct Gen {
     return "    sgm::cluster_sync();\n";
   }
 
+  // one-barrier push flush for small tiles (two receive buffers of CL slots each)
+  static constexpr i64 kPushBudget = 32 * 1024;
+  static i64 pad4(i64 n) { return (n + 3) / 4 * 4; }
+  bool push_flush(const std::vector<int>& fl) const {
+    if (CL <= 1) return false;
+    i64 b = 0;
+    for (int f : fl) b += 2 * CL * pad4(prod4(nodes[f].sl)) * ec;
+    return b <= kPushBudget;
+  }
+
   void emit_flush(const std::vector<int>& fl, int pos) {
+    if (push_flush(fl)) {
+      for (int f : fl) {
+        const Node& x = nodes[f];
+        const u32 keep = (u32)(CL - 1) & ~x.pend;
+        const i64 szp = pad4(prod4(x.sl));
+        os << "    sgm::cl_push<N, " << prod4(x.sl) << ", " << szp << ", " << CL << ", " << keep << "u, NT>("
+           << tile_ptr(f) << ", (C*)(sm + " << flush_tmp_off.at({pos, f}) << ") + (cit & 1u) * " << CL * szp
+           << ", crank);\n";
+      }
+      os << cl_sync();
+      os << "  SGM_TR(" << 3000 + 4 * pos + 1 << ");\n";
+      for (int f : fl) {
+        const Node& x = nodes[f];
+        const u32 keep = (u32)(CL - 1) & ~x.pend;
+        const i64 szp = pad4(prod4(x.sl));
+        os << "    sgm::cl_gather<N, " << prod4(x.sl) << ", " << szp << ", " << CL << ", " << keep << "u, NT>("
+           << tile_ptr(f) << ", (const C*)(sm + " << flush_tmp_off.at({pos, f}) << ") + (cit & 1u) * " << CL * szp
+           << ", crank);\n";
+      }
+      os << "    sgm::csync<NT>();\n";
+      os << "  SGM_TR(" << 3000 + 4 * pos + 3 << ");\n";
+      return;
+    }
     // reduce-scatter (DSMEM loads into tmp) + all-gather (DSMEM stores)
     os << cl_sync();
     os << "  SGM_TR(" << 3000 + 4 * pos + 1 << ");\n";

@@ -1035,12 +1035,16 @@ __device__ __forceinline__ void mm_stream_f32_core(float* __restrict__ out, cons
       for (int kc = 0; kc < NKC; ++kc) {
         const u32 slot = ring_wait<S>(full, q);
         const float* st = reinterpret_cast<const float*>(ring + slot * SLOT);
-#pragma unroll 4
-        for (int k = kl; k < KC; k += KL) {
-          const float4 w0 = *reinterpret_cast<const float4*>(st + k * BW + cg * 4);
-          const float4 w1 = *reinterpret_cast<const float4*>(st + k * BW + BW / 2 + cg * 4);
+        // k-rows kl, kl+KL, ... of the stage, software-pipelined one step ahead so
+        // the shared-memory loads of step i+1 overlap the 8*M FMAs of step i (a
+        // plain loop left the FMAs waiting on LDS: short-scoreboard stalls in ncu)
+        constexpr int NI = (KC + KL - 1) / KL;
+        auto load = [&](int i, float4& w0, float4& w1, float* av) {
+          const int k = kl + i * KL;
+          if (KC % KL != 0 && k >= KC) return;
+          w0 = *reinterpret_cast<const float4*>(st + k * BW + cg * 4);
+          w1 = *reinterpret_cast<const float4*>(st + k * BW + BW / 2 + cg * 4);
           const float* ak = pa + (i64)(kc * KC + k) * M;
-          float av[M];
           if constexpr (M % 4 == 0) {
 #pragma unroll
             for (int u = 0; u < M / 4; ++u) *reinterpret_cast<float4*>(&av[u * 4]) = *reinterpret_cast<const float4*>(ak + u * 4);
@@ -1048,13 +1052,30 @@ __device__ __forceinline__ void mm_stream_f32_core(float* __restrict__ out, cons
 #pragma unroll
             for (int m = 0; m < M; ++m) av[m] = ak[m];
           }
+        };
+        float4 w0, w1;
+        float av[M];
+        load(0, w0, w1, av);
 #pragma unroll
-          for (int m = 0; m < M; ++m) {
-            acc[m][0] = fmaf(av[m], w0.x, acc[m][0]); acc[m][1] = fmaf(av[m], w0.y, acc[m][1]);
-            acc[m][2] = fmaf(av[m], w0.z, acc[m][2]); acc[m][3] = fmaf(av[m], w0.w, acc[m][3]);
-            acc[m][4] = fmaf(av[m], w1.x, acc[m][4]); acc[m][5] = fmaf(av[m], w1.y, acc[m][5]);
-            acc[m][6] = fmaf(av[m], w1.z, acc[m][6]); acc[m][7] = fmaf(av[m], w1.w, acc[m][7]);
+        for (int i = 0; i < NI; ++i) {
+          float4 n0 = w0, n1 = w1;
+          float nav[M];
+#pragma unroll
+          for (int m = 0; m < M; ++m) nav[m] = av[m];
+          if (i + 1 < NI) load(i + 1, n0, n1, nav);
+          if (KC % KL == 0 || kl + i * KL < KC) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              acc[m][0] = fmaf(av[m], w0.x, acc[m][0]); acc[m][1] = fmaf(av[m], w0.y, acc[m][1]);
+              acc[m][2] = fmaf(av[m], w0.z, acc[m][2]); acc[m][3] = fmaf(av[m], w0.w, acc[m][3]);
+              acc[m][4] = fmaf(av[m], w1.x, acc[m][4]); acc[m][5] = fmaf(av[m], w1.y, acc[m][5]);
+              acc[m][6] = fmaf(av[m], w1.z, acc[m][6]); acc[m][7] = fmaf(av[m], w1.w, acc[m][7]);
+            }
           }
+          w0 = n0;
+          w1 = n1;
+#pragma unroll
+          for (int m = 0; m < M; ++m) av[m] = nav[m];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
@@ -1231,6 +1252,46 @@ __device__ __noinline__ void cl_rs_phase2(typename N::C* tile, const typename N:
 #pragma unroll
     for (u32 r = 0; r < (u32)CL; ++r)
       if (((r ^ me) & KEEP) == 0u) const_cast<typename N::C*>(peer_ptr(tile, r))[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster all-reduce of a small partial tile with ONE cluster barrier (push
+// model): every CTA writes its partial into slot `me` of each group peer's
+// receive buffer (same smem offset in every CTA), barrier, then each CTA sums
+// the group's slots in rank order (its own slot read from its tile), so every
+// CTA ends with the identical, fixed-order sum -- the same order as the
+// reduce-scatter form.  The caller alternates two receive buffers between
+// consecutive items, so a buffer is rewritten only after a later barrier.
+template <class N, int SZ, int SZP, int CL, u32 KEEP, int NT>
+__device__ __forceinline__ void cl_push(const typename N::C* __restrict__ tile, typename N::C* rbuf, u32 me) {
+  typedef typename N::C C;
+  constexpr int VW = 16 / sizeof(C);
+  constexpr int NV = SZ / VW;
+  for (int v = threadIdx.x; v < NV; v += NT) {
+    union { uint4 q; C c[VW]; } u;
+#pragma unroll
+    for (int i = 0; i < VW; ++i) u.c[i] = tile[v * VW + i];
+#pragma unroll
+    for (u32 r = 0; r < (u32)CL; ++r)
+      if (r != me && ((r ^ me) & KEEP) == 0u)
+        *reinterpret_cast<uint4*>(const_cast<C*>(peer_ptr(rbuf + me * SZP + v * VW, r))) = u.q;
+  }
+  for (int e = NV * VW + threadIdx.x; e < SZ; e += NT)
+#pragma unroll
+    for (u32 r = 0; r < (u32)CL; ++r)
+      if (r != me && ((r ^ me) & KEEP) == 0u) const_cast<C*>(peer_ptr(rbuf + me * SZP + e, r))[0] = tile[e];
+}
+
+template <class N, int SZ, int SZP, int CL, u32 KEEP, int NT>
+__device__ __forceinline__ void cl_gather(typename N::C* __restrict__ tile, const typename N::C* rbuf, u32 me) {
+  typedef typename N::A Acc;
+  for (int e = threadIdx.x; e < SZ; e += NT) {
+    Acc acc = N::azero();
+#pragma unroll
+    for (u32 r = 0; r < (u32)CL; ++r)
+      if (((r ^ me) & KEEP) == 0u) N::aadd(acc, r == me ? tile[e] : rbuf[r * SZP + e]);
+    tile[e] = N::fin(acc);
   }
 }
 

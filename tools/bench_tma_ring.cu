@@ -41,6 +41,7 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, int c0, 
 
 struct Cfg {
   int box_n, box_k, slots, boxes_per_stage, split_k;  // split_k: CTAs share columns by splitting K
+  int es = 2;                                         // element bytes
 };
 
 // Work: column tiles of (box_n * boxes_per_stage) columns x K rows; units = column tiles x split_k.
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(64) ring_kernel(const __grid_constant__ CUtens
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) u64 full[16], empty[16];
   unsigned char* ring = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
-  const int stage_bytes = cfg.box_n * 2 * cfg.box_k * cfg.boxes_per_stage;
+  const int stage_bytes = cfg.box_n * cfg.es * cfg.box_k * cfg.boxes_per_stage;
   const int tile_cols = cfg.box_n * cfg.boxes_per_stage;
   const int ntiles = N / tile_cols;
   const int units = ntiles * cfg.split_k;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(64) ring_kernel(const __grid_constant__ CUtens
         if (q >= (u32)cfg.slots) mbar_wait(&empty[slot], ((q / cfg.slots) - 1) & 1);
         mbar_expect_tx(&full[slot], stage_bytes);
         for (int b = 0; b < cfg.boxes_per_stage; ++b)
-          tma2d(ring + slot * stage_bytes + b * cfg.box_n * 2 * cfg.box_k, &tm, tile * tile_cols + b * cfg.box_n,
+          tma2d(ring + slot * stage_bytes + b * cfg.box_n * cfg.es * cfg.box_k, &tm, tile * tile_cols + b * cfg.box_n,
                 ks * kper + s * cfg.box_k, &full[slot]);
       }
     }
@@ -88,7 +89,50 @@ __global__ void __launch_bounds__(64) ring_kernel(const __grid_constant__ CUtens
   }
 }
 
-int main() {
+// f32 vs bf16 box shapes at one CTA per SM, 4 x 32 KB stages (argv[1] == "dtype")
+static void dtype_sweep(void* w, size_t bytes, unsigned long long* sink, int sms) {
+  struct DC { const char* name; CUtensorMapDataType dt; int es; int box_n; CUtensorMapSwizzle sw; int bps; };
+  const DC cs[] = {{"bf16 64x128 SW128 x2", CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, 2},
+                   {"f32  64x128 none   x1", CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 64, CU_TENSOR_MAP_SWIZZLE_NONE, 1},
+                   {"f32  32x128 SW128  x2", CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 32, CU_TENSOR_MAP_SWIZZLE_128B, 2},
+                   {"f32  32x128 none   x2", CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 32, CU_TENSOR_MAP_SWIZZLE_NONE, 2}};
+  for (const DC& c : cs)
+    for (int cps : {1, 2}) {
+      const int K = 4096;
+      const int N = (int)(bytes / ((size_t)K * c.es));
+      const int slots = cps == 1 ? 4 : 3;
+      const int slot_bytes = cps == 1 ? 32768 : 16384;
+      const int bps = cps == 1 ? c.bps : (c.bps > 1 ? c.bps / 2 : 1);
+      const int box_k = slot_bytes / (bps * c.box_n * c.es);
+      if (box_k > 256) continue;
+      CUtensorMap tm;
+      cuuint64_t gdim[2] = {(cuuint64_t)N, (cuuint64_t)K};
+      cuuint64_t gstr[1] = {(cuuint64_t)N * c.es};
+      cuuint32_t box[2] = {(cuuint32_t)c.box_n, (cuuint32_t)box_k};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = cuTensorMapEncodeTiled(&tm, c.dt, 2, w, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, c.sw,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) { printf("%s encode failed %d\n", c.name, (int)r); continue; }
+      Cfg cfg{c.box_n, box_k, slots, bps, 1, c.es};
+      const int smem = slot_bytes * slots + 1024;
+      cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      const int grid = sms * cps;
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      for (int i = 0; i < 3; ++i) ring_kernel<<<grid, 64, smem>>>(tm, K, N, cfg, sink);
+      cudaEventRecord(e0);
+      for (int i = 0; i < 20; ++i) ring_kernel<<<grid, 64, smem>>>(tm, K, N, cfg, sink);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("%s ctas/SM %d slots %dx%dK: %.1f us  %.0f GB/s %s\n", c.name, cps, slots, slot_bytes / 1024, ms * 50.0,
+             bytes / (ms * 50.0) / 1e3, cudaGetErrorString(cudaGetLastError()));
+    }
+}
+
+int main(int argc, char** argv) {
   const int K = 4096, N = 28672;  // two 4096 x 14336 bf16 weights side by side (235 MB)
   size_t bytes = (size_t)K * N * 2;
   void* w;
@@ -98,6 +142,7 @@ int main() {
   cudaMalloc(&sink, 8);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 1) { dtype_sweep(w, bytes, sink, sms); return 0; }
   std::vector<Cfg> cfgs;
   for (int box_k : {32, 64, 128, 256})
     for (int slots : {4, 8, 12})
