@@ -111,7 +111,8 @@ def test_best_kernels_deployment_dtype(S):
     best = json.load(open(path))
     for w, b in best.items():
         pop = P.load_population(w)
-        u = next(x for x in P.units(pop) if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"])
+        u = next(x for x in P.units(pop) if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"]
+                 and pop["candidates"][x.pair]["template_id"] == b.get("template", pop["candidates"][x.pair]["template_id"]))
         dt = pop["dtype"]
         rng = np.random.default_rng(11)
         prog = pop["program"]
@@ -122,3 +123,31 @@ def test_best_kernels_deployment_dtype(S):
         got = S.run_concrete(u.cand, ins, dtype=dt, hints=hints)
         for name in prog["outputs"]:
             assert S.rel_err(got[name], exp[name]) < TOL[dt], w
+
+
+@pytest.mark.parametrize("w,template,mapping,params", [
+    ("R", 26, "O.1.x,W.1.x", {"x": 2, "i": 1}),   # RMS statistic reduced across a cluster mid-kernel
+    ("G", 0, "O.1.x,Wgate.1.x,Wup.1.x", {"x": 8, "i": 1}),
+    ("A", 42, "Kt.1.x,O.1.x,Q.1.x,V.1.x", {"x": 2, "i": 1}),
+])
+@pytest.mark.parametrize("hints", [{}, {"one_cta": 1}, {"max_cluster": 4, "max_gsplit": 1}, {"max_cluster": 1},
+                                   {"variant": 2}])
+def test_physical_plan_variants_deployment_dtype(S, w, template, mapping, params, hints):
+    """One candidate under the physical plans the tuner picks between: two CTAs per
+    SM (tcgen05, TMEM halves), one per SM, cluster reductions (one-barrier push for
+    small partials, reduce-scatter for large), gsplit tail reductions."""
+    from oracle import block_np
+    from paper_2604_15272_b200 import population as P
+    pop = P.load_population(w)
+    u = next(x for x in P.units(pop) if x.cand.mapping_list() == sorted(mapping.split(",")) and x.cand.params == params
+             and pop["candidates"][x.pair]["template_id"] == template)
+    dt = pop["dtype"]
+    rng = np.random.default_rng(13)
+    prog = pop["program"]
+    ins = {t["name"]: _round(rng.standard_normal(tuple(t["dims"])), dt) for t in prog["tensors"] if t["role"] == "input"}
+    exp = block_np.run_program(prog, ins)
+    got = S.run_concrete(u.cand, ins, dtype=dt, hints=hints)
+    got2 = S.run_concrete(u.cand, ins, dtype=dt, hints=hints)  # second launch: self-resetting counters, buffer parity
+    for name in prog["outputs"]:
+        assert S.rel_err(got[name], exp[name]) < TOL[dt], (w, hints)
+        assert np.array_equal(np.asarray(got[name]), np.asarray(got2[name])), (w, hints)
