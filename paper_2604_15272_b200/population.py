@@ -191,7 +191,20 @@ class WorkloadContext:
             self.ff_inputs = ff_fill_inputs(self.program, seed64, device)
             self.ff_expected = ff_run(ir.program_candidate(self.program), self.ff_inputs, device)
             self.ff_out = [torch().empty_like(x) for x in self.ff_expected]
+        self._ff_lanes = None
         self.bytes = algorithmic_bytes(pop)
+
+    FF_STREAMS = 8
+
+    def ff_lanes(self) -> list:
+        """(stream, outputs) pairs for concurrent FF checks: the checks are
+        verification, not timing, so candidates whose kernels leave SMs idle
+        (small grids, serial loops) overlap on side streams."""
+        if self._ff_lanes is None:
+            t = torch()
+            self._ff_lanes = [(t.cuda.Stream(device=self.device), [t.empty_like(x) for x in self.ff_expected])
+                              for _ in range(self.FF_STREAMS)]
+        return self._ff_lanes
 
     def refresh_expected(self) -> None:
         """Re-run the program in GF(p) on the current FF inputs (into ff_expected)."""
@@ -290,15 +303,31 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
     L = _abi.lib()
     rot = ctx.ws.rot
     plans = [None] * n
+    if ff:
+        # FF checks first, spread over side streams (they overlap where kernels leave
+        # SMs idle), then joined, so the timing passes below run alone on the GPU
+        main = t.cuda.current_stream(dev)
+        lanes = ctx.ff_lanes()
+        for sl, _ in lanes:
+            sl.wait_stream(main)
+        for k, u in enumerate(us):
+            sl, outs = lanes[k % len(lanes)]
+            try:
+                PLANS.get(u.cand, _abi.FF, None, dev).run(ctx.ff_inputs, outs, stream=sl.cuda_stream)
+                sp = C.c_void_p(sl.cuda_stream)
+                for g, e in zip(outs, ctx.ff_expected):
+                    _abi.check(L.sgm_compare_u32_acc(C.c_void_p(g.data_ptr()), C.c_void_p(e.data_ptr()), g.numel(),
+                                                     sp, C.c_void_p(counters.data_ptr() + 8 * k)))
+            except Exception as exc:
+                recs[k].error = f"{type(exc).__name__}: {str(exc)[:300]}"
+        for sl, _ in lanes:
+            main.wait_stream(sl)
     timer = Timer(n, dev)
     for k, u in enumerate(us):
         rec = recs[k]
+        if rec.error is not None:
+            continue
         try:
-            if ff:
-                PLANS.get(u.cand, _abi.FF, None, dev).run(ctx.ff_inputs, ctx.ff_out)
-                for g, e in zip(ctx.ff_out, ctx.ff_expected):
-                    _abi.check(L.sgm_compare_u32_acc(C.c_void_p(g.data_ptr()), C.c_void_p(e.data_ptr()), g.numel(),
-                                                     stream, C.c_void_p(counters.data_ptr() + 8 * k)))
             plan = plans[k] = PLANS.get(u.cand, ctx.numsys, None, dev)
             # screening: one launch on its own input set (streams from HBM), no warm-up;
             # it only ranks candidates for the rotation pass
