@@ -1154,7 +1154,9 @@ struct Gen {
             x.kc = 8;
             while (x.kc * 2 <= kmax && K % (x.kc * 2) == 0) x.kc *= 2;
             i64 a0 = (a.sl[0] > 1) ? x.sl[0] : 1, a1 = (a.sl[1] > 1) ? x.sl[1] : 1;
-            x.at_bytes = a0 * a1 * K * M * 4;
+            // mm_stream_f32 reads a single-batch row-major A in place (DIRECT)
+            const bool direct = a0 * a1 == 1 && a.store != ST_VIEW;
+            x.at_bytes = direct ? 0 : a0 * a1 * K * M * 4;
             x.red_bytes = (i64)(NT / 32) * M * 64 * 4;
           }
         }

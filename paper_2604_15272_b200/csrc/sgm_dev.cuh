@@ -1012,18 +1012,24 @@ __device__ __forceinline__ void mm_stream_f32_core(float* __restrict__ out, cons
                 (BW & (BW - 1)) == 0, "mm_stream_f32 shape");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cg = lane % CGN, kq = lane / CGN, kl = warp * KQ + kq;
-  // k-major copy of A: at[ab][k][m]
-  for (int e = tid; e < A0 * A1 * K * M; e += NT) {
-    const int m = e % M;
-    const int k = (e / M) % K;
-    const int ab = e / (M * K);
-    const int a1 = ab % A1, a0 = ab / A1;
-    at[e] = A[a0 * SA0 + a1 * SA1 + (i64)m * SA2 + (i64)k * SA3];
+  // DIRECT (one A batch, unit k stride): read A[m][k] in place (M scalar loads
+  // per k, each a broadcast across a k-lane's column groups), saving the K*M
+  // k-major copy -- shared memory the ring gets instead (more bytes in flight)
+  constexpr bool DIRECT = SA3 == 1 && A0 * A1 == 1;
+  if constexpr (!DIRECT) {
+    // k-major copy of A: at[ab][k][m]
+    for (int e = tid; e < A0 * A1 * K * M; e += NT) {
+      const int m = e % M;
+      const int k = (e / M) % K;
+      const int ab = e / (M * K);
+      const int a1 = ab % A1, a0 = ab / A1;
+      at[e] = A[a0 * SA0 + a1 * SA1 + (i64)m * SA2 + (i64)k * SA3];
+    }
+    csync<NT>();
   }
-  csync<NT>();
   for (int bi = 0; bi < B0 * B1; ++bi) {
     const int b1 = bi % B1, b0 = bi / B1;
-    const float* pa = at + (i64)((SA0 ? b0 : 0) * A1 + (SA1 ? b1 : 0)) * K * M;
+    const float* pa = DIRECT ? A : at + (i64)((SA0 ? b0 : 0) * A1 + (SA1 ? b1 : 0)) * K * M;
 #pragma unroll 1
     for (int t = 0; t < NTB; ++t) {
       float acc[M][8];
@@ -1044,6 +1050,11 @@ __device__ __forceinline__ void mm_stream_f32_core(float* __restrict__ out, cons
           if (KC % KL != 0 && k >= KC) return;
           w0 = *reinterpret_cast<const float4*>(st + k * BW + cg * 4);
           w1 = *reinterpret_cast<const float4*>(st + k * BW + BW / 2 + cg * 4);
+          if constexpr (DIRECT) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) av[m] = pa[(i64)m * SA2 + kc * KC + k];
+            return;
+          }
           const float* ak = pa + (i64)(kc * KC + k) * M;
           if constexpr (M % 4 == 0) {
 #pragma unroll
