@@ -124,7 +124,8 @@ typedef struct {
   int32_t variant;         /* v > 0: the v-th best split the planner scored (physical-plan tuning) */
   int32_t one_cta;         /* 1: size the TMA ring for one CTA per SM (32 KB slots) */
   int32_t max_gsplit;      /* cap on gsplit parts per reduction group (0 = none) */
-  int32_t _reserved[4];
+  int32_t slot_kb;         /* TMA ring slot size in KB at one CTA per SM: 0 = planner (32), 16 = twice the slots */
+  int32_t _reserved[3];
 } sgm_plan_hints;
 
 typedef struct {

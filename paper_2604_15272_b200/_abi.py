@@ -39,8 +39,8 @@ class PlanHints(C.Structure):
         ("max_cluster", C.c_int32), ("target_ctas", C.c_int32), ("threads", C.c_int32),
         ("smem_budget", C.c_int32), ("no_loop_split", C.c_int32), ("no_hoist", C.c_int32),
         ("use_tcgen05", C.c_int32), ("no_tma", C.c_int32), ("trace", C.c_int32),
-        ("variant", C.c_int32), ("one_cta", C.c_int32), ("max_gsplit", C.c_int32),
-        ("_reserved", C.c_int32 * 4),
+        ("variant", C.c_int32), ("one_cta", C.c_int32), ("max_gsplit", C.c_int32), ("slot_kb", C.c_int32),
+        ("_reserved", C.c_int32 * 3),
     ]
 
 

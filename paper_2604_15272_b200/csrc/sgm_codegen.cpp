@@ -1511,7 +1511,13 @@ struct Gen {
       int S2 = (110 * 1024 - base - 1024 - stg) / 16384;
       if (S2 >= 3) { slotB = 16384; S = std::min(6, S2); paired = true; }
     }
-    if (S < 3) { slotB = 16384; S = std::min(12, (kSmemCap - base - 1024 - stg) / slotB); }
+    // 16 KB slots at one CTA per SM (hint): twice the slots for the same bytes, so
+    // small boxes (LoRA's 16-column X@A stages) do not each hold a 32 KB slot
+    // while the big stream waits behind them
+    if (S < 3 || (!paired && d.hints.slot_kb == 16)) {
+      slotB = 16384;
+      S = std::min(12, (kSmemCap - base - 1024 - stg) / slotB);
+    }
     for (auto& x : nodes) {
       if (x.kind != SGM_MATMUL || !x.tma) continue;
       if (x.tc) while (x.kc * 256 > slotB) x.kc /= 2;

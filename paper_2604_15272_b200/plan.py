@@ -129,6 +129,7 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.variant = int(h.get("variant", 0))
     d.hints.one_cta = int(h.get("one_cta", 0))
     d.hints.max_gsplit = int(h.get("max_gsplit", 0))
+    d.hints.slot_kb = int(h.get("slot_kb", 0))
     return d
 
 

@@ -399,7 +399,8 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
 VARIANT_HINTS = [{}] + [{"variant": v} for v in range(1, 6)] + [{"one_cta": 1}] + \
     [{"one_cta": 1, "variant": v} for v in range(1, 4)] + \
     [{"max_gsplit": g} for g in (1, 2, 4)] + [{"max_gsplit": g, "one_cta": 1} for g in (1, 2, 4)] + \
-    [{"max_gsplit": g, "max_cluster": 1} for g in (1, 2, 4)] + [{"max_cluster": 1}, {"max_cluster": 2}]
+    [{"max_gsplit": g, "max_cluster": 1} for g in (1, 2, 4)] + [{"max_cluster": 1}, {"max_cluster": 2}] + \
+    [{"one_cta": 1, "slot_kb": 16}, {"slot_kb": 16}]
 
 
 def precompile_variants(units: list, numsys: int, threads: int = 0) -> None:
