@@ -194,7 +194,7 @@ class WorkloadContext:
         self._ff_lanes = None
         self.bytes = algorithmic_bytes(pop)
 
-    FF_STREAMS = 8
+    FF_STREAMS = int(os.environ.get("SGM_FF_STREAMS", "8"))
 
     def ff_lanes(self) -> list:
         """(stream, outputs) pairs for concurrent FF checks: the checks are
