@@ -1134,6 +1134,9 @@ struct Gen {
             ++ntma;
             x.tc = true;
             x.kc = K % 128 == 0 ? 128 : (K % 64 == 0 ? 64 : (K % 32 == 0 ? 32 : 16));
+            // narrow tiles (NN <= 64, one 64-column box per stage) take up to 256 k-rows
+            // per stage: a 16-column LoRA X@A stage otherwise held a whole slot for 4 KB
+            if (NN <= 64 && K % 256 == 0) x.kc = 256;
             x.xb_shared = x.sl[0] * x.sl[1] == 1;
             x.at_bytes = x.xb_shared ? 0 : 32 * K;
             x.red_bytes = 0;
@@ -1520,7 +1523,7 @@ struct Gen {
     }
     for (auto& x : nodes) {
       if (x.kind != SGM_MATMUL || !x.tma) continue;
-      if (x.tc) while (x.kc * 256 > slotB) x.kc /= 2;
+      if (x.tc) while (x.kc * (x.sl[3] <= 64 ? 128 : 256) > slotB) x.kc /= 2;
       else while (x.kc * x.bw * 4 > slotB) x.kc /= 2;
     }
     if (paired)  // half of TMEM per CTA: fewer independent accumulators

@@ -914,7 +914,12 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
   constexpr u32 IDESC = UMMA_IDESC_BF16_M128_N16;
   constexpr int NMMA = K / 16;                      // MMAs per tile
   constexpr int AC = ACC < NMMA ? ACC : NMMA;        // accumulators actually written
-  static_assert(K % KC == 0 && KC % 16 == 0 && KC * 256 <= SLOT && M <= 16 && NTL * ACC * 16 <= 512,
+  // narrow tile (NN <= 64): one 64-column box per stage; the MMA's second 64-row
+  // half re-reads the first (LBO 0) and its results are discarded in the epilogue
+  constexpr bool NARROW = NN <= 64;
+  constexpr u32 LBO = NARROW ? 0u : (u32)(KC * 128);
+  static_assert(K % KC == 0 && KC % 16 == 0 && KC * (NARROW ? 128 : 256) <= SLOT && M <= 16 &&
+                    NTL * ACC * 16 <= 512,
                 "mm_stream_tc shape");
   static_assert(BUILD || B0 * B1 == 1, "a prebuilt A^T covers one batch");
   u16* xb = reinterpret_cast<u16*>(xbuf);
@@ -939,7 +944,7 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
           const u32 st = smem_u32(ring + slot * SLOT);
 #pragma unroll
           for (int ks = 0; ks < KC / 16; ++ks) {
-            const u64 ad = umma_desc_sw128(st + ks * 2048, KC * 128, 1024);
+            const u64 ad = umma_desc_sw128(st + ks * 2048, LBO, 1024);
             const u64 bd = umma_desc(xs + ((kc * KC + ks * 16) >> 3) * 256, 256, 128);
             const int g = kc * (KC / 16) + ks;  // MMA index along K
             umma_bf16(tmem + (t * ACC + g % AC) * 16, ad, bd, IDESC, g >= AC);
