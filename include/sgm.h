@@ -177,6 +177,13 @@ int sgm_set_cache_dir(const char* path);
 /* Validate + plan + generate + compile (or cache-hit) a candidate kernel. */
 int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out);
 int sgm_plan_info_get(const sgm_plan* plan, sgm_plan_info* info);
+/* The B200 resource model without compiling: validate + plan + generate only.
+ * SGM_OK iff the candidate has a feasible physical plan on this device (shared
+ * memory <= 227 KB per CTA incl. the TMA ring, TMEM columns, cluster size <= 16,
+ * TMA box limits, scratch); `info` (may be NULL) receives the plan (no
+ * compile_ms / cache_hit).  Replaces the reference's 2-byte / 164 KiB budget
+ * filter (tuner.py:36-37,67-71) for backend "b200". */
+int sgm_plan_feasible(const sgm_plan_desc* desc, sgm_plan_info* info);
 /* Copy the generated CUDA source (NUL-terminated, truncated to cap). Returns length via *len. */
 int sgm_plan_source(const sgm_plan* plan, char* buf, size_t cap, size_t* len);
 int sgm_plan_destroy(sgm_plan* plan);
@@ -229,6 +236,18 @@ int sgm_compare_u32_acc(const uint32_t* a, const uint32_t* b, int64_t n, void* s
  * numsys selects the element type of both buffers (F64/F32/BF16). */
 int sgm_rel_err(const void* a, const void* b, int64_t n, int numsys, void* stream,
                 double* out);
+/* Asynchronous, mixed-type rel_err accumulation (the sweep's deployment-dtype
+ * parity gate): `a` holds n elements of number system `numsys` (F64/F32/BF16),
+ * `b` n fp64 values.  Folds into dev_slot[0..2] (device uint64, zeroed by the
+ * caller): [0] max|a-b| and [1] max|b| as non-negative double bit patterns
+ * (atomicMax), [2] += count of non-finite elements of a.  The host computes
+ * rel_err = slot[2] ? inf : slot[0] / (1 + slot[1]), as interp.py:228-231. */
+int sgm_rel_err_acc(const void* a, int numsys, const double* b, int64_t n, void* stream, uint64_t* dev_slot);
+/* Programmatic dependent launch for every later launch (and graph capture):
+ * 1 on (default unless the SGM_NO_PDL environment variable is set), 0 off.
+ * With PDL a launch may begin while the previous kernel in the stream drains;
+ * generated kernels gate every global access on griddepcontrol.wait. */
+int sgm_set_pdl(int on);
 /* Fill with a standard-normal-like deterministic pattern (for timing inputs). */
 int sgm_fill_normal(void* dst, int64_t n, int numsys, uint64_t seed, void* stream);
 

@@ -82,14 +82,17 @@ def hash_op(kind: str, x) -> np.ndarray:
 
 
 def matmul(a, b) -> np.ndarray:
-    """Exact (a @ b) mod p with numpy int64: split a into 11-bit limbs so no
-    partial sum overflows (limb * residue < 2^42, K < 2^21)."""
+    """Exact (a @ b) mod p.  Both operands are split into 11-bit limbs and the
+    9 limb products run as float64 BLAS GEMMs: every partial sum is an integer
+    below K * 2^22 < 2^53 (K < 2^31), so the float result is exact."""
     a, b = reduce(a), reduce(b)
     out = np.zeros(np.broadcast_shapes(a.shape[:-2], b.shape[:-2]) + (a.shape[-2], b.shape[-1]), dtype=np.int64)
-    for shift in (0, 11, 22):
-        limb = (a >> shift) & 0x7FF
-        part = (limb @ b) % P
-        out = (out + part * pow(2, shift, P)) % P
+    al = [((a >> s) & 0x7FF).astype(np.float64) for s in (0, 11, 22)]
+    bl = [((b >> s) & 0x7FF).astype(np.float64) for s in (0, 11, 22)]
+    for i in range(3):
+        for j in range(3):
+            part = np.matmul(al[i], bl[j]).astype(np.int64) % P
+            out = (out + part * pow(2, 11 * (i + j), P)) % P
     return out
 
 

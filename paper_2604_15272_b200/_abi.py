@@ -73,6 +73,7 @@ SYMBOLS = {
     "sgm_init": ([C.c_int], C.c_int),
     "sgm_set_cache_dir": ([C.c_char_p], C.c_int),
     "sgm_plan_create": ([C.POINTER(PlanDesc), C.POINTER(C.c_void_p)], C.c_int),
+    "sgm_plan_feasible": ([C.POINTER(PlanDesc), C.POINTER(PlanInfo)], C.c_int),
     "sgm_plan_info_get": ([C.c_void_p, C.POINTER(PlanInfo)], C.c_int),
     "sgm_plan_source": ([C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     "sgm_plan_destroy": ([C.c_void_p], C.c_int),
@@ -90,6 +91,8 @@ SYMBOLS = {
     "sgm_ff_fill": ([C.c_void_p, C.c_int64, C.c_uint64, C.c_uint64, C.c_void_p], C.c_int),
     "sgm_compare_u32": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "sgm_rel_err": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.POINTER(C.c_double)], C.c_int),
+    "sgm_set_pdl": ([C.c_int], C.c_int),
+    "sgm_rel_err_acc": ([C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p], C.c_int),
     "sgm_fill_normal": ([C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_void_p], C.c_int),
 }
 

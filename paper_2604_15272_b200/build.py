@@ -68,6 +68,35 @@ def nvcc_check(out_dir: str | None = None) -> str:
     return cubin
 
 
+REF_SRC = "/root/reference/pkg"
+REF_DST = os.path.join(ROOT, "baseline", "_ref")
+
+
+def install_reference(force: bool = False) -> str | None:
+    """Install the UNMODIFIED reference package (symfuse, incl. its compiled Cython
+    e-graph core) into baseline/_ref, offline, from a /tmp copy of /root/reference/pkg
+    (the mount is read-only and the build writes into the source tree).  `--no-deps`:
+    numpy is importable but not in the wheelhouse.  baseline/_ref is git-ignored but
+    travels to the GPU box with the snapshot; on the box /root/reference is absent,
+    so an existing install is kept and nothing is attempted."""
+    if not force and os.path.isdir(os.path.join(REF_DST, "symfuse")):
+        return REF_DST
+    if not os.path.isdir(REF_SRC):
+        return None
+    import shutil
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="symfuse_src_")
+    try:
+        src = os.path.join(tmp, "pkg")
+        shutil.copytree(REF_SRC, src, ignore=shutil.ignore_patterns("__pycache__", "*.so", "build"))
+        _run([sys.executable, "-m", "pip", "install", "-q", "--no-index", "--no-build-isolation", "--no-deps",
+              "--find-links", "/opt/wheelhouse", "--upgrade", "--target", REF_DST, src])
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    return REF_DST
+
+
 if __name__ == "__main__":
     print(build_lib(force="--force" in sys.argv))
     print(nvcc_check())
+    print(install_reference())

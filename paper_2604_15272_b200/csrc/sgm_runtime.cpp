@@ -183,7 +183,7 @@ struct DevState {
   int sms = 148;
   int cc_major = 10, cc_minor = 0;
   CUmodule util = nullptr;
-  CUfunction f_fill64, f_fill32, f_fill16, f_ff_fill, f_cmp, f_re64, f_re32, f_re16, f_n64, f_n32, f_n16;
+  CUfunction f_fill64, f_fill32, f_fill16, f_ff_fill, f_cmp, f_re64, f_re32, f_re16, f_rex32, f_rex16, f_n64, f_n32, f_n16;
   CUdeviceptr red = 0;  // 4 x u64 reduction scratch
   // host-buffer (e2e) staging shared by every plan of this device: pinned host
   // memory + one device buffer, grown on demand (sgm_plan_run_host)
@@ -272,9 +272,19 @@ int compile_cubin(const std::string& src, std::string& cubin, double& ms, int& h
   const char* hnames[2] = {"sgm_dev.cuh", "sgm_util.cuh"};
   if (nvrtcCreateProgram(&prog, src.c_str(), "sgm_kernel.cu", 2, hdrs, hnames) != NVRTC_SUCCESS)
     return set_err(SGM_ERR_NVRTC, "nvrtcCreateProgram failed");
-  const char* opts[] = {kArch, "-std=c++17", "-lineinfo", "-DNDEBUG", "--extra-device-vectorization",
-                        "-diag-suppress=177,550"};
-  nvrtcResult r = nvrtcCompileProgram(prog, 6, opts);
+  std::vector<const char*> opts = {kArch, "-std=c++17", "-lineinfo", "-DNDEBUG", "--extra-device-vectorization",
+                                   "-diag-suppress=177,550"};
+  static std::vector<std::string> extra = [] {  // experiments: SGM_NVRTC_OPTS="-a -b"
+    std::vector<std::string> v;
+    if (const char* e = getenv("SGM_NVRTC_OPTS")) {
+      std::istringstream ss(e);
+      std::string w;
+      while (ss >> w) v.push_back(w);
+    }
+    return v;
+  }();
+  for (auto& e : extra) opts.push_back(e.c_str());
+  nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
   if (r != NVRTC_SUCCESS) {
     size_t ls = 0;
     nvrtcGetProgramLogSize(prog, &ls);
@@ -342,7 +352,19 @@ struct sgm_plan {
   CUgraphExec gexec = nullptr;
   std::vector<const void*> graph_key;
   int graph_rot = 0;
+  int graph_pdl = -1;        // PDL setting the cached graph was captured with
 };
+
+// programmatic dependent launch: on unless SGM_NO_PDL is set; sgm_set_pdl overrides
+static std::atomic<int> g_pdl{-1};
+static bool pdl_on() {
+  int v = g_pdl.load();
+  if (v < 0) {
+    v = getenv("SGM_NO_PDL") == nullptr ? 1 : 0;
+    g_pdl.store(v);
+  }
+  return v != 0;
+}
 
 struct sgm_timer {
   int cap = 0;
@@ -394,6 +416,8 @@ int sgm_init(int device) {
     CU(D.cuModuleGetFunction(&S.f_re64, S.util, "sgm_relerr_f64"));
     CU(D.cuModuleGetFunction(&S.f_re32, S.util, "sgm_relerr_f32"));
     CU(D.cuModuleGetFunction(&S.f_re16, S.util, "sgm_relerr_bf16"));
+    CU(D.cuModuleGetFunction(&S.f_rex32, S.util, "sgm_relerr_x_f32"));
+    CU(D.cuModuleGetFunction(&S.f_rex16, S.util, "sgm_relerr_x_bf16"));
     CU(D.cuModuleGetFunction(&S.f_n64, S.util, "sgm_normal_f64"));
     CU(D.cuModuleGetFunction(&S.f_n32, S.util, "sgm_normal_f32"));
     CU(D.cuModuleGetFunction(&S.f_n16, S.util, "sgm_normal_bf16"));
@@ -515,6 +539,29 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
   return SGM_OK;
 }
 
+int sgm_plan_feasible(const sgm_plan_desc* desc, sgm_plan_info* info) {
+  if (!desc) return set_err(SGM_ERR_INVALID, "null argument");
+  int sms = (t_device >= 0 && g_dev[t_device].init) ? g_dev[t_device].sms : 148;
+  sgmcg::GenResult gr = sgmcg::generate(*desc, sms);
+  if (gr.status != SGM_OK) return set_err(gr.status, "%s", gr.error.c_str());
+  if (info) {
+    memset(info, 0, sizeof *info);
+    info->logical_blocks = gr.logical_blocks;
+    info->ctas = gr.ctas;
+    info->cluster = gr.cluster;
+    info->threads = gr.threads;
+    info->smem_bytes = gr.smem_bytes;
+    info->loop_parts = gr.loop_parts;
+    info->free_parts = gr.free_parts;
+    info->scratch_bytes = gr.scratch_bytes;
+    info->n_tcgen05 = gr.n_tcgen05;
+    info->source_hash = sgmcg::fnv1a(gr.source);
+    snprintf(info->kernel_name, sizeof info->kernel_name, "%s", gr.kernel_name.c_str());
+    snprintf(info->plan_summary, sizeof info->plan_summary, "%s", gr.summary.c_str());
+  }
+  return SGM_OK;
+}
+
 int sgm_plan_info_get(const sgm_plan* p, sgm_plan_info* info) {
   if (!p || !info) return set_err(SGM_ERR_INVALID, "null argument");
   memset(info, 0, sizeof *info);
@@ -625,8 +672,7 @@ static int launch_plan(sgm_plan* p, const void* const* inputs, void* const* outp
   for (int k = 0; k < p->n_out; ++k) args.out[k] = outputs[k];
   args.scratch = (void*)p->scratch;
   void* params[] = {&args};
-  static const bool pdl = getenv("SGM_NO_PDL") == nullptr;
-  if (pdl && D.cuLaunchKernelEx) {
+  if (pdl_on() && D.cuLaunchKernelEx) {
     // programmatic stream serialization: this grid may launch while the previous
     // kernel in the stream drains; the generated code's griddepcontrol.wait keeps
     // every global access after that kernel's completion
@@ -752,7 +798,8 @@ int sgm_plan_time(sgm_plan* p, const void* const* inputs, void* const* outputs, 
 static int plan_graph(sgm_plan* p, const void* const* inputs, void* const* outputs, int rot) {
   std::vector<const void*> key(inputs, inputs + (size_t)rot * p->n_in);
   key.insert(key.end(), outputs, outputs + p->n_out);
-  if (p->gexec && p->graph_rot == rot && key == p->graph_key) return SGM_OK;
+  const int pdl = pdl_on() ? 1 : 0;
+  if (p->gexec && p->graph_rot == rot && p->graph_pdl == pdl && key == p->graph_key) return SGM_OK;
   if (p->gexec) { D.cuGraphExecDestroy(p->gexec); p->gexec = nullptr; }
   if (p->graph) { D.cuGraphDestroy(p->graph); p->graph = nullptr; }
   if (!p->tstream) CU(D.cuStreamCreate(&p->tstream, CU_STREAM_NON_BLOCKING));
@@ -768,6 +815,7 @@ static int plan_graph(sgm_plan* p, const void* const* inputs, void* const* outpu
   p->graph = g;
   p->graph_key = key;
   p->graph_rot = rot;
+  p->graph_pdl = pdl;
   return SGM_OK;
 }
 
@@ -888,6 +936,22 @@ int sgm_rel_err(const void* a, const void* b, int64_t n, int numsys, void* strea
   memcpy(&mb, &r[1], 8);
   *out = r[2] ? INFINITY : md / (1.0 + mb);
   return SGM_OK;
+}
+
+int sgm_set_pdl(int on) {
+  g_pdl.store(on ? 1 : 0);
+  return SGM_OK;
+}
+
+int sgm_rel_err_acc(const void* a, int numsys, const double* b, int64_t n, void* stream, uint64_t* dev_slot) {
+  int st = ensure_ctx();
+  if (st) return st;
+  DevState& S = g_dev[t_device];
+  if (numsys == SGM_FF) return set_err(SGM_ERR_INVALID, "rel_err is undefined for finite-field buffers");
+  CUdeviceptr pa = (CUdeviceptr)a, pb = (CUdeviceptr)b, pc = (CUdeviceptr)dev_slot;
+  void* args[] = {&pa, &pb, &n, &pc};
+  CUfunction f = numsys == SGM_F64 ? S.f_re64 : numsys == SGM_BF16 ? S.f_rex16 : S.f_rex32;
+  return launch_1d(f, n, (CUstream)stream, args);
 }
 
 int sgm_fill_normal(void* dst, int64_t n, int numsys, uint64_t seed, void* stream) {

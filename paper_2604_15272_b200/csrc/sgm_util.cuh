@@ -30,7 +30,7 @@ template <class T> __device__ __forceinline__ double to_d(T v) { return (double)
 template <> __device__ __forceinline__ double to_d<u16>(u16 v) { return (double)__uint_as_float(((u32)v) << 16); }
 
 // out[0] = max|a-b| (double bits), out[1] = max|b|, out[2] = #non-finite in a
-template <class T> __device__ void relerr_impl(const T* a, const T* b, i64 n, u64* out) {
+template <class T, class U> __device__ void relerr_impl(const T* a, const U* b, i64 n, u64* out) {
   double md = 0.0, mb = 0.0;
   u64 bad = 0;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
@@ -53,6 +53,9 @@ template <class T> __device__ void relerr_impl(const T* a, const T* b, i64 n, u6
 extern "C" __global__ void sgm_relerr_f64(const double* a, const double* b, i64 n, u64* out) { relerr_impl(a, b, n, out); }
 extern "C" __global__ void sgm_relerr_f32(const float* a, const float* b, i64 n, u64* out) { relerr_impl(a, b, n, out); }
 extern "C" __global__ void sgm_relerr_bf16(const u16* a, const u16* b, i64 n, u64* out) { relerr_impl(a, b, n, out); }
+// deployment-dtype output `a` against an fp64 expectation `b` (the parity gate of the sweep)
+extern "C" __global__ void sgm_relerr_x_f32(const float* a, const double* b, i64 n, u64* out) { relerr_impl(a, b, n, out); }
+extern "C" __global__ void sgm_relerr_x_bf16(const u16* a, const double* b, i64 n, u64* out) { relerr_impl(a, b, n, out); }
 
 // deterministic standard-normal-like values (Box-Muller on hashed counters)
 template <class N> __device__ void normal_impl(typename N::S* dst, i64 n, u64 seed) {

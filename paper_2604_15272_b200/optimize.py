@@ -1,0 +1,158 @@
+"""End-to-end optimisation run (BASELINE config 5; the paper's "total
+optimisation time"; reference driver cli.py:69-196).
+
+Per workload, timed stage by stage:
+
+  search   the UNCHANGED reference stages 1-3 (template generation, mapping
+           enumeration, e-graph verification; cli.py:77-157) on a host process
+           pool (search.parallel_search); rank 0 searches, the
+           population is broadcast to the other ranks
+  space    every verified pair's divisibility-only parameter space
+           (tuner.enumerate_param_space, budget None; G at 14336 through the
+           plan layer)
+  compile  this rank's shard of the population, cold: NVRTC with an empty
+           cubin cache, host threads split evenly between ranks
+  sweep    population.evaluate_workload: FF check + CUDA-event profile of
+           every candidate, deployment-dtype parity gate on the contenders,
+           1000-launch refine of the top 3
+  argmin   per workload across ranks (NCCL all_reduce(MIN), population.reduce_best)
+
+Nothing is read from the committed populations: they are only compared with the
+live search (`matches_committed`).
+"""
+from __future__ import annotations
+
+import os
+import time
+from typing import Optional
+
+from . import population as P
+from . import workloads as W
+
+
+def _bcast(obj, dist, src: int = 0):
+    if dist is None:
+        return obj
+    box = [obj]
+    dist.broadcast_object_list(box, src=src)
+    return box[0]
+
+
+def _max(x: float, dist, device) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64,
+                     device=f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def population_of(run, name: str) -> tuple:
+    """Wait for one workload of a search.SearchRun; (population, search stats)."""
+    t0 = time.perf_counter()
+    rep = run.result(name)
+    waited = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pop = W.population_from_report(name, rep, rep["timings"]["wall_s"], graphs=rep["graphs"])
+    tm = rep["timings"]
+    out = dict(search_s=tm["generate_s"] + tm["verify_tail_s"], generate_s=tm["generate_s"],
+               verify_tail_s=tm["verify_tail_s"], mappings_cpu_s=tm["mappings_cpu_s"],
+               verify_cpu_s=tm["verify_cpu_s"], ready_at_s=tm["wall_s"], waited_s=waited,
+               space_s=time.perf_counter() - t0, templates=len(rep["templates"]),
+               mapping_candidates=rep["stats"]["mapping_candidates"], verified_pairs=rep["stats"]["verified_pairs"])
+    try:
+        com = P.load_population(name)
+        out["matches_committed"] = [(c["template_id"], c["mapping"], c["space"]) for c in pop["candidates"]] == \
+            [(c["template_id"], c["mapping"], c["space"]) for c in com["candidates"]]
+    except FileNotFoundError:
+        out["matches_committed"] = None
+    return pop, out
+
+
+def search_workload(name: str, workers: Optional[int] = None) -> tuple:
+    """Stages 1-3 + parameter spaces of one workload on host processes (forks:
+    call before CUDA is initialised).  Returns (population, stats)."""
+    from .search import SearchRun
+    run = SearchRun([name], workers)
+    try:
+        return population_of(run, name)
+    finally:
+        run.close()
+
+
+# evaluation order: short searches first, so the GPU work of those overlaps the long ones
+EVAL_ORDER = ("G", "L", "R", "A", "Q")
+
+
+def start_search(workloads, workers: Optional[int] = None):
+    """Rank 0, before CUDA is initialised: every workload's search starts now,
+    concurrently (search.SearchRun); evaluate_all consumes them as they finish."""
+    from .search import SearchRun
+    return SearchRun(list(workloads), workers)
+
+
+def evaluate_population(pop: dict, device: int, dist=None, refine_top: int = 3) -> dict:
+    """Cold compile of this rank's shard + the sweep + the cross-rank argmin."""
+    import torch
+    from . import _abi
+    rank = dist.get_rank() if dist is not None else 0
+    world = dist.get_world_size() if dist is not None else 1
+    us = P.units(pop)
+    mine = P.shard(us, rank, world)
+    numsys = P.numsys_of(pop["dtype"])
+    threads = max(1, (os.cpu_count() or 8) // world)
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    errs = P.precompile([u.cand for u in mine], [numsys, _abi.FF], device, threads=threads)
+    t_compile = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ctx = P.WorkloadContext(pop, device)
+    recs = P.evaluate_workload(ctx, mine, refine_top=refine_top)
+    torch.cuda.synchronize(device)
+    t_sweep = time.perf_counter() - t0
+    best = P.argmin(recs)
+    win = P.reduce_best(best, dist)
+    out = dict(candidates=len(us), candidates_this_rank=len(mine), compile_threads=threads,
+               compile_s=_max(t_compile, dist, device), sweep_s=_max(t_sweep, dist, device),
+               compile_errors=sum(1 for e in errs.values() if e),
+               ff_mismatch=sum(1 for r in recs if r.ff_ok is False), winner_index=win)
+    if best is not None and best.index == win:
+        out["winner"] = {"latency_us": best.latency_us, "mapping": best.mapping, "params": best.params,
+                         "dep_err": best.dep_err, "dep_ok": best.dep_ok, "timing": best.timing,
+                         "kernel": (best.plan or {}).get("kernel_name")}
+    return out
+
+
+def evaluate_all(run, workloads, device: int, dist=None, refine_top: int = 3, log=None) -> dict:
+    """Compile + sweep every workload as soon as its search is done (rank 0 owns
+    the SearchRun and broadcasts each population); returns per-workload stage
+    times and the wall time of the whole optimisation run (search start to the
+    last argmin), the figure the paper reports per workload."""
+    t_start = run.t0 if run is not None else time.perf_counter()
+    order = [w for w in EVAL_ORDER if w in workloads] + [w for w in workloads if w not in EVAL_ORDER]
+    per = {}
+    for w in order:
+        item = population_of(run, w) if run is not None else None
+        pop, st = _bcast(item, dist)
+        ev = evaluate_population(pop, device, dist, refine_top)
+        r = {**st, **ev}
+        r["total_s"] = st["search_s"] + st["space_s"] + ev["compile_s"] + ev["sweep_s"]
+        r["done_at_s"] = _max(time.perf_counter() - t_start, dist, device)
+        per[w] = r
+        if log:
+            log(f"e2e-opt {w}: search {st['search_s']:.1f}s (ready at {st['ready_at_s']:.1f}s), compile "
+                f"{ev['compile_s']:.1f}s, sweep {ev['sweep_s']:.1f}s -> done at {r['done_at_s']:.1f}s; "
+                f"{ev['candidates']} candidates, matches committed: {st['matches_committed']}")
+    if run is not None:
+        run.close()
+    n = sum(r["candidates"] for r in per.values())
+    cold = sum(r["compile_s"] + r["sweep_s"] for r in per.values())
+    wall = max(r["done_at_s"] for r in per.values())
+    return {"per_workload": per, "wall_s": wall,
+            "e2e_opt_s": {w: r["total_s"] for w, r in per.items()},
+            "search_s": sum(r["search_s"] + r["space_s"] for r in per.values()),
+            "compile_s": sum(r["compile_s"] for r in per.values()),
+            "sweep_s": sum(r["sweep_s"] for r in per.values()),
+            "candidates": n, "cold_candidates_per_s": n / cold if cold > 0 else None,
+            "end_to_end_candidates_per_s": n / wall}

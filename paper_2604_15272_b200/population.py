@@ -72,6 +72,18 @@ def units(pop: dict) -> list:
     return out
 
 
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+
+def hbm_peak_gbs() -> float:
+    """Measured HBM copy bandwidth of this pool's B200s (MEASURED_PEAKS.json, driver-written)."""
+    try:
+        with open(os.path.join(os.path.dirname(HERE), "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return FALLBACK_HBM_GBS
+
+
 def algorithmic_bytes(pop: dict) -> int:
     """Unique HBM traffic of the workload: every input read once, every output written once."""
     es = DTYPE_BYTES[pop["dtype"]]
@@ -170,6 +182,15 @@ class Record:
     timing: str = ""
     variant: int = 0
     hints: dict = field(default_factory=dict)
+    dep_err: Optional[float] = None   # deployment-dtype rel_err vs the fp64 program (parity gate)
+    dep_ok: Optional[bool] = None
+
+
+# Deployment-dtype tolerances of the parity gate (north star item 4), the same
+# bars as tests/test_gpu_numerics.py: bf16 storage / fp32 accumulation 1e-2
+# (output rounding 2^-8 plus bf16 MMA operands), fp32 1e-5.  rel_err is the
+# reference's max|a-b| / (1 + max|b|) (interp.py:228-231).
+DEP_TOL = {_abi.BF16: 1e-2, _abi.F32: 1e-5, _abi.F64: 1e-9}
 
 
 class WorkloadContext:
@@ -206,6 +227,21 @@ class WorkloadContext:
                               for _ in range(self.FF_STREAMS)]
         return self._ff_lanes
 
+    def deployment_expected(self) -> list:
+        """fp64 program outputs on input set 0 of the deployment-dtype workspace
+        (the rounded bf16/fp32 values, widened exactly), computed once on the
+        device by the program lowered to a one-block candidate (interp.py:69-83)."""
+        if getattr(self, "_dep_exp", None) is None:
+            t = torch()
+            ins = [x.to(t.float64) for x in self.ws.sets[0]]
+            outs = [t.empty(tuple(self.program.spec(n).dims), dtype=t.float64, device=self.device)
+                    for n in self.program.outputs]
+            PLANS.get(ir.program_candidate(self.program), _abi.F64, None, self.device).run(ins, outs)
+            del ins
+            self._dep_exp = outs
+            self._dep_out = [t.empty_like(o, dtype=torch_dtype(self.numsys)) for o in outs]
+        return self._dep_exp
+
     def refresh_expected(self) -> None:
         """Re-run the program in GF(p) on the current FF inputs (into ff_expected)."""
         from .ff import ff_run
@@ -238,6 +274,45 @@ def evaluate_unit(ctx: WorkloadContext, u: Unit, budget_us: float = 2000.0, max_
     except Exception as exc:
         rec.error = f"{type(exc).__name__}: {str(exc)[:300]}"
     return rec
+
+
+def deployment_check(ctx: "WorkloadContext", plans: list) -> list:
+    """The parity gate: run each plan (the exact kernel that is timed: candidate,
+    number system and physical-plan hints) once in the deployment dtype on input
+    set 0 and fold its rel_err against the fp64 program into a device slot.
+    One host read for the whole batch.  Returns [(rel_err, ok)] (tolerance DEP_TOL)."""
+    import ctypes as C
+    t = torch()
+    if not plans:
+        return []
+    exp = ctx.deployment_expected()
+    outs = ctx._dep_out
+    n_out = len(exp)
+    slots = t.zeros((len(plans), n_out, 3), dtype=t.int64, device=ctx.device)
+    s = t.cuda.current_stream(ctx.device).cuda_stream
+    L = _abi.lib()
+    failed = set()
+    for k, pl in enumerate(plans):
+        try:
+            pl.run(ctx.ws.sets[0], outs, init_outputs=True)
+            for j, (o, e) in enumerate(zip(outs, exp)):
+                _abi.check(L.sgm_rel_err_acc(C.c_void_p(o.data_ptr()), pl.numsys, C.c_void_p(e.data_ptr()), o.numel(),
+                                             C.c_void_p(s), C.c_void_p(slots[k, j].data_ptr())))
+        except Exception:
+            failed.add(k)
+    raw = slots.cpu().numpy()
+    tol = DEP_TOL[ctx.numsys]
+    res = []
+    for k in range(len(plans)):
+        if k in failed:
+            res.append((float("inf"), False))
+            continue
+        err = 0.0
+        for j in range(n_out):
+            md, mb = raw[k, j, :2].view(np.float64)
+            err = max(err, float("inf") if raw[k, j, 2] else float(md / (1.0 + mb)))
+        res.append((err, bool(err <= tol)))
+    return res
 
 
 class Timer:
@@ -360,6 +435,11 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
         for j, k in enumerate(sel):
             recs[k].latency_us = lat2[j]
             recs[k].timing = "rotation"
+        # parity gate: every contender's deployment-dtype kernel (the one just timed)
+        # against the fp64 program; a candidate that fails cannot win
+        for k, (err, good) in zip(sel, deployment_check(ctx, [plans[k] for k in sel])):
+            recs[k].dep_err, recs[k].dep_ok = err, good
+        sel = [k for k in sel if recs[k].dep_ok]
         top = sorted(sel, key=lambda k: (recs[k].latency_us, recs[k].index))[:refine_top]
         # physical-plan tuning: planner variants of the top candidates (the FF check of
         # the candidate covers every variant: each is the same block graph, re-split)
@@ -380,6 +460,10 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
             for j, (k, v, pl) in enumerate(vp):
                 if 0 < latv[j] < best_plan[k][0]:
                     best_plan[k] = (latv[j], v, pl)
+        swapped = [k for k in top if best_plan[k][1] != 0]
+        for k, (err, good) in zip(swapped, deployment_check(ctx, [best_plan[k][2] for k in swapped])):
+            if not good:  # a physical variant that breaks numerics falls back to the checked plan
+                best_plan[k] = (recs[k].latency_us, 0, plans[k])
         timer = Timer(len(top), dev)
         for j, k in enumerate(top):
             timer.enqueue(j, best_plan[k][2], ctx.ws.sets, ctx.ws.outputs, reps=max(1, -(-refine_launches // rot)))
@@ -450,11 +534,64 @@ def tune_physical(ctx: "WorkloadContext", u: Unit, launches: int = 1000) -> tupl
     return best, h, p
 
 
+def ff_check_plan(ctx: "WorkloadContext", cand: ir.Candidate, hints: Optional[dict]) -> bool:
+    """Finite-field check of one physical variant: the candidate compiled with the
+    same planner hints (splits, gsplit/cluster caps) in GF(p), bit-exact against
+    the program's FF output."""
+    from .ff import ff_equal
+    t = torch()
+    outs = [t.empty_like(e) for e in ctx.ff_expected]
+    PLANS.get(cand, _abi.FF, hints or None, ctx.device).run(ctx.ff_inputs, outs)
+    return all(ff_equal(g, e) for g, e in zip(outs, ctx.ff_expected))
+
+
+def graph_latency(ctx: "WorkloadContext", plan: Plan, launches: int = 1000, pdl: bool = True) -> float:
+    """Mean microseconds per launch over `launches` back-to-back launches (CUDA
+    graphs of one rotation of input sets, every launch misses L2), with
+    programmatic dependent launch on or off for the capture."""
+    _abi.bind_device(ctx.device)
+    _abi.check(_abi.lib().sgm_set_pdl(1 if pdl else 0))
+    try:
+        timer = Timer(1, ctx.device)
+        timer.enqueue(0, plan, ctx.ws.sets, ctx.ws.outputs, reps=max(1, -(-launches // ctx.ws.rot)))
+        us = timer.read(1)[0]
+        timer.close()
+    finally:
+        _abi.check(_abi.lib().sgm_set_pdl(1))
+    return us
+
+
+def isolated_latency(ctx: "WorkloadContext", plan: Plan, launches: int = 50) -> dict:
+    """Single-launch latency with nothing to overlap: before every launch a
+    256 MB read (a reduction over a buffer twice the L2) leaves L2 holding only
+    clean lines of other data, and the launch is bracketed by its own CUDA
+    events on the launching stream, so launch processing, prologue and tail are
+    all inside the number (no CUDA graph; the next launch cannot start early).
+    Returns mean/median/min microseconds."""
+    t = torch()
+    flush = t.zeros(64 << 20, dtype=t.float32, device=ctx.device)
+    evs = [(t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)) for _ in range(launches)]
+    rot = ctx.ws.rot
+    sink = []
+    for k, (a, b) in enumerate(evs):
+        sink.append(flush.sum())
+        a.record()
+        plan.run(ctx.ws.sets[k % rot], ctx.ws.outputs, init_outputs=False)
+        b.record()
+    t.cuda.synchronize(ctx.device)
+    us = sorted(a.elapsed_time(b) * 1000.0 for a, b in evs)
+    return {"mean_us": sum(us) / len(us), "median_us": us[len(us) // 2], "min_us": us[0], "launches": launches,
+            "method": "per-launch CUDA events, 256 MB read-only L2 flush between launches, no graph"}
+
+
 def argmin(records: list) -> Optional[Record]:
-    ok = [r for r in records if r.error is None and r.latency_us is not None and r.ff_ok is not False]
+    """Fastest candidate that passed the FF check and, among those, the
+    deployment-dtype parity gate (records the gate never saw rank after)."""
+    ok = [r for r in records if r.error is None and r.latency_us is not None and r.ff_ok is not False
+          and r.dep_ok is not False]
     if not ok:
         return None
-    return min(ok, key=lambda r: (r.latency_us, r.index))
+    return min(ok, key=lambda r: (r.dep_ok is not True, r.latency_us, r.index))
 
 
 def reduce_best(best: Optional[Record], dist) -> int:

@@ -21,11 +21,16 @@ from typing import Optional
 import numpy as np
 
 from . import _abi, ir
-from .errors import EmptyParamSpaceError, NonIntegerError
+from .errors import EmptyParamSpaceError, NonIntegerError, SymfuseError
 from .plan import PLANS, numsys_of, torch, torch_dtype
 
 DEFAULT_BUDGET = 164 * 1024
 ELEMENT_BYTES = 2
+# budget_bytes sentinel: keep a point iff this backend's planner finds a feasible
+# physical plan for it (sgm_plan_feasible: 227 KB smem incl. the TMA ring, TMEM
+# columns, cluster <= 16, TMA boxes, scratch) instead of the reference's
+# "sum of all tiles x 2 B <= 164 KiB" (tuner.py:36-37,67-71)
+B200_BUDGET = "b200"
 L2_BYTES = 126 * 1024 * 1024
 
 
@@ -53,10 +58,11 @@ def smem_usage(graph, mapping=None, params=None) -> int:
     return sum(prod(s) for s in ir.concrete_shapes(c).values()) * ELEMENT_BYTES
 
 
-def enumerate_param_space(graph, mapping=None, budget_bytes: Optional[int] = DEFAULT_BUDGET) -> list:
+def enumerate_param_space(graph, mapping=None, budget_bytes=DEFAULT_BUDGET, *, dtype=np.float32) -> list:
     """Power-of-two sizes per parallel dim up to the smallest extent it splits
     (1 if it splits nothing), kept if divisible and within the budget; in
-    lexicographic order over (grid dims..., loop)."""
+    lexicographic order over (grid dims..., loop).  budget_bytes=B200_BUDGET
+    keeps the points the B200 planner can realise in `dtype` instead."""
     c = _cand(graph, mapping)
     names = list(c.block.pdims)
     axes = []
@@ -73,9 +79,23 @@ def enumerate_param_space(graph, mapping=None, budget_bytes: Optional[int] = DEF
             usage = smem_usage(c.with_params(params))
         except NonIntegerError:
             continue
-        if budget_bytes is None or usage <= budget_bytes:
+        if budget_bytes == B200_BUDGET:
+            if plan_feasible(c.with_params(params), numsys_of(dtype)):
+                space.append(params)
+        elif budget_bytes is None or usage <= budget_bytes:
             space.append(params)
     return space
+
+
+def plan_feasible(cand: ir.Candidate, numsys: int, hints: Optional[dict] = None) -> bool:
+    """True iff the planner finds a physical plan for the candidate (no compile, no device)."""
+    import ctypes as C
+    from .plan import build_desc
+    try:
+        desc = build_desc(cand, numsys, hints)
+    except (SymfuseError, ValueError):
+        return False
+    return _abi.lib().sgm_plan_feasible(C.byref(desc), None) == 0
 
 
 @dataclass(frozen=True)
@@ -172,11 +192,17 @@ class ProfileResult:
 
 
 def tune(graph, mapping, backend: str = "cost", samples: int = 16, seed: int = 0,
-         budget_bytes: Optional[int] = DEFAULT_BUDGET, trials: int = 3, model: CostModel = CostModel(), *,
+         budget_bytes=DEFAULT_BUDGET, trials: int = 3, model: CostModel = CostModel(), *,
          dtype=np.float32, device: Optional[int] = None) -> ProfileResult:
-    """tuner.py:188-224 with backend "b200" (GPU profiler) added."""
+    """tuner.py:188-224 with backend "b200" (GPU profiler) added.  For "b200" the
+    reference's default budget (DEFAULT_BUDGET, the 2-byte / 164 KiB model that
+    empties most full-scale spaces) is replaced by the B200 resource
+    model (B200_BUDGET); an explicit other budget is honoured.  The sampled
+    points are compiled in parallel before they are timed in `dtype`."""
     c = _cand(graph, mapping)
-    space = enumerate_param_space(c, budget_bytes=budget_bytes)
+    if backend == "b200" and budget_bytes == DEFAULT_BUDGET:
+        budget_bytes = B200_BUDGET
+    space = enumerate_param_space(c, budget_bytes=budget_bytes, dtype=dtype)
     if not space:
         raise EmptyParamSpaceError(c.program.name)
     names = list(c.block.pdims)
@@ -187,6 +213,19 @@ def tune(graph, mapping, backend: str = "cost", samples: int = 16, seed: int = 0
         points = [space[i] for i in picked]
     else:
         points = space
+    if backend == "b200":
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        from .plan import Plan
+        ns = numsys_of(dtype)
+
+        def compile_only(params):
+            try:
+                Plan(c.with_params(params), ns, None, None).close()
+            except Exception:
+                pass  # re-raised by the timed call below
+        with ThreadPoolExecutor(min(16, os.cpu_count() or 4)) as ex:
+            list(ex.map(compile_only, points))
     best = None
     for params in points:
         cc = c.with_params(params)
