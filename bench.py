@@ -247,6 +247,8 @@ def main() -> None:
                     help="skip the end-to-end optimisation run (live search + cold compile + first sweep)")
     ap.add_argument("--search-workers", type=int, default=0, help="host processes for the parallel search")
     ap.add_argument("--records", default=None, help="write all records (JSON) here (rank 0)")
+    ap.add_argument("--report", default=None,
+                    help="directory: per-workload sweep report (reference format + GPU evidence) and DOT files (rank 0)")
     ap.add_argument("--best-out", default=None, help="write the tuned best kernel per workload (JSON) here")
     args = ap.parse_args()
     args.workloads = [w for w in args.workloads.split(",") if w]
@@ -325,6 +327,8 @@ def main() -> None:
         errs = sum(1 for r in recs if r.error)
         log("step " + " ".join(f"{w}:{t:.2f}s" for w, t in t_w.items()) + f" errors={errs}")
         for r in recs:
+            r.gpu_rank = rank
+        for r in recs:
             if r.error:
                 log(f"  error {r.workload}#{r.index} {r.params} {r.error[:160]}")
                 break
@@ -371,6 +375,12 @@ def main() -> None:
         dist.all_gather_object(gathered, [r.__dict__ for r in recs])
         all_recs = [P.Record(**d) for part in gathered for d in part]
 
+    if args.report and rank == 0:
+        for w in args.workloads:
+            rep = P.report(pops[w], [r for r in all_recs if r.workload == w])
+            os.makedirs(args.report, exist_ok=True)
+            P.write_report(rep, os.path.join(args.report, f"report_{w}.json"))
+            P.export_dots(pops[w], rep, os.path.join(args.report, f"dot_{w}"))
     if args.records and rank == 0:
         with open(args.records, "w") as fh:
             json.dump([r.__dict__ for r in all_recs], fh)

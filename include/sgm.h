@@ -125,7 +125,8 @@ typedef struct {
   int32_t one_cta;         /* 1: size the TMA ring for one CTA per SM (32 KB slots) */
   int32_t max_gsplit;      /* cap on gsplit parts per reduction group (0 = none) */
   int32_t slot_kb;         /* TMA ring slot size in KB at one CTA per SM: 0 = planner (32), 16 = twice the slots */
-  int32_t _reserved[3];
+  int32_t wd_test;         /* test only: 1 = the TMA producer issues nothing, so the watchdog must fire */
+  int32_t _reserved[2];
 } sgm_plan_hints;
 
 typedef struct {
@@ -243,6 +244,14 @@ int sgm_rel_err(const void* a, const void* b, int64_t n, int numsys, void* strea
  * (atomicMax), [2] += count of non-finite elements of a.  The host computes
  * rel_err = slot[2] ? inf : slot[0] / (1 + slot[1]), as interp.py:228-231. */
 int sgm_rel_err_acc(const void* a, int numsys, const double* b, int64_t n, void* stream, uint64_t* dev_slot);
+/* Watchdog of a plan's kernel: generated kernels bound every wait on an
+ * asynchronous completion (TMA bytes, MMA commits, remote cluster arrivals) to
+ * 0.5 s; a wait that times out sets a flag in the plan's module and gives up,
+ * so a broken kernel terminates (with wrong results) instead of hanging the
+ * device.  Synchronises `stream`, sets *tripped = 1 if any launch since the
+ * last reset timed out, and clears the flag when `reset` != 0.  The Python
+ * layer reports it as the reference's "run: ..." verdict (interp.py:278-281). */
+int sgm_plan_watchdog(sgm_plan* plan, void* stream, int reset, int* tripped);
 /* Programmatic dependent launch for every later launch (and graph capture):
  * 1 on (default unless the SGM_NO_PDL environment variable is set), 0 off.
  * With PDL a launch may begin while the previous kernel in the stream drains;

@@ -40,7 +40,7 @@ class PlanHints(C.Structure):
         ("smem_budget", C.c_int32), ("no_loop_split", C.c_int32), ("no_hoist", C.c_int32),
         ("use_tcgen05", C.c_int32), ("no_tma", C.c_int32), ("trace", C.c_int32),
         ("variant", C.c_int32), ("one_cta", C.c_int32), ("max_gsplit", C.c_int32), ("slot_kb", C.c_int32),
-        ("_reserved", C.c_int32 * 3),
+        ("wd_test", C.c_int32), ("_reserved", C.c_int32 * 2),
     ]
 
 
@@ -91,6 +91,7 @@ SYMBOLS = {
     "sgm_ff_fill": ([C.c_void_p, C.c_int64, C.c_uint64, C.c_uint64, C.c_void_p], C.c_int),
     "sgm_compare_u32": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "sgm_rel_err": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.POINTER(C.c_double)], C.c_int),
+    "sgm_plan_watchdog": ([C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_int)], C.c_int),
     "sgm_set_pdl": ([C.c_int], C.c_int),
     "sgm_rel_err_acc": ([C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p], C.c_int),
     "sgm_fill_normal": ([C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_void_p], C.c_int),

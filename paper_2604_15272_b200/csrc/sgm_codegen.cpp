@@ -1659,6 +1659,7 @@ struct Gen {
     // prologue (measured: a few % faster than holding it back so the prologue's
     // loads do not queue behind TMA traffic; SGM_LATE_STREAM=1 restores the wait)
     os << "    if (tid == NT) {\n      unsigned pq = 0;\n";
+    if (d.hints.wd_test) os << "      return;  // wd_test: nothing is streamed, every ring wait must time out\n";
     if (getenv("SGM_LATE_STREAM")) os << "      sgm::mbar_wait(go, 0);\n";
     os << "      unsigned pit = 0;\n";
     os << "      for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl, ++pit) {\n";

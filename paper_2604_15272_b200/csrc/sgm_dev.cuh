@@ -559,11 +559,39 @@ __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_gene
 __device__ __forceinline__ void mbar_init(u64* b, u32 cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(u64* b, u32 parity) {
+// Watchdog (per module): every wait on an asynchronous completion (TMA
+// transaction bytes, MMA commits, remote cluster arrivals) is bounded.  A wait
+// that exceeds SGM_WD_NS sets sgm_wd_flag and gives up, so a broken candidate
+// ends (with garbage) instead of hanging the GPU; the runtime reads the flag
+// (sgm_plan_watchdog) and the sweep records "run: timeout" (interp.py:278-281).
+#ifndef SGM_WD_NS
+#define SGM_WD_NS 500000000ull
+#endif
+__device__ unsigned sgm_wd_flag;
+__device__ __forceinline__ u64 wd_now() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __noinline__ void wd_trip() { atomicOr(&sgm_wd_flag, 1u); }
+__device__ __forceinline__ bool mbar_try(u64* b, u32 parity) {
+  u32 ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ void mbar_wait_slow(u64* b, u32 parity) {
+  if (*(volatile unsigned*)&sgm_wd_flag) return;  // already timed out: drain without waiting
+  const u64 t0 = wd_now();
+  while (!mbar_try(b, parity))
+    if (wd_now() - t0 > SGM_WD_NS) { wd_trip(); return; }
+}
+__device__ __forceinline__ void mbar_wait(u64* b, u32 parity) {
+  if (!mbar_try(b, parity)) mbar_wait_slow(b, parity);
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -1208,13 +1236,16 @@ template <int NT, int CL> __device__ __noinline__ void cl_barrier_core(u64* bar,
   }
   if (threadIdx.x == 0) {
     u32 ok = 0;
-    while (!ok)
+    const u64 t0 = wd_now();
+    while (!ok) {
+      if (wd_now() - t0 > SGM_WD_NS) { wd_trip(); break; }
       asm volatile(
           "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
           "selp.u32 %0, 1, 0, P1;\n\t}"
           : "=r"(ok)
           : "r"(smem_u32(bar)), "r"(phase)
           : "memory");
+    }
   }
   csync<NT>();
 }

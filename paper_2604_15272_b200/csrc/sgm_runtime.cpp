@@ -81,6 +81,7 @@ struct Driver {
   SGM_FN(cuModuleLoadData, CUmodule*, const void*)
   SGM_FN(cuModuleUnload, CUmodule)
   SGM_FN(cuModuleGetFunction, CUfunction*, CUmodule, const char*)
+  SGM_FN(cuModuleGetGlobal, CUdeviceptr*, size_t*, CUmodule, const char*)
   SGM_FN(cuFuncSetAttribute, CUfunction, CUfunction_attribute, int)
   SGM_FN(cuFuncGetAttribute, int*, CUfunction_attribute, CUfunction)
   SGM_FN(cuLaunchKernel, CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
@@ -138,6 +139,7 @@ struct Driver {
     g &= sym(cuModuleLoadData, "cuModuleLoadData");
     g &= sym(cuModuleUnload, "cuModuleUnload");
     g &= sym(cuModuleGetFunction, "cuModuleGetFunction");
+    g &= sym(cuModuleGetGlobal, "cuModuleGetGlobal_v2");
     g &= sym(cuFuncSetAttribute, "cuFuncSetAttribute");
     g &= sym(cuFuncGetAttribute, "cuFuncGetAttribute");
     g &= sym(cuLaunchKernel, "cuLaunchKernel");
@@ -353,6 +355,7 @@ struct sgm_plan {
   std::vector<const void*> graph_key;
   int graph_rot = 0;
   int graph_pdl = -1;        // PDL setting the cached graph was captured with
+  CUdeviceptr wd_flag = 0;   // the module's sgm_wd_flag (watchdog, sgm_dev.cuh)
 };
 
 // programmatic dependent launch: on unless SGM_NO_PDL is set; sgm_set_pdl overrides
@@ -467,6 +470,10 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
   if (r != CUDA_SUCCESS) { delete p; return cu_check(r, "cuModuleLoadData"); }
   r = D.cuModuleGetFunction(&p->fn, p->mod, gr.kernel_name.c_str());
   if (r != CUDA_SUCCESS) { sgm_plan_destroy(p); return cu_check(r, "cuModuleGetFunction"); }
+  {
+    size_t wsz = 0;
+    if (D.cuModuleGetGlobal(&p->wd_flag, &wsz, p->mod, "sgm_wd_flag") != CUDA_SUCCESS) p->wd_flag = 0;
+  }
   // prefer the largest shared-memory carveout: the planner counts on two CTAs per SM
   // at ~110 KB each, which the default carveout does not always grant
   D.cuFuncSetAttribute(p->fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
@@ -935,6 +942,24 @@ int sgm_rel_err(const void* a, const void* b, int64_t n, int numsys, void* strea
   memcpy(&md, &r[0], 8);
   memcpy(&mb, &r[1], 8);
   *out = r[2] ? INFINITY : md / (1.0 + mb);
+  return SGM_OK;
+}
+
+int sgm_plan_watchdog(sgm_plan* p, void* stream, int reset, int* tripped) {
+  if (!p || !p->fn || !tripped) return set_err(SGM_ERR_INVALID, "null plan / no device");
+  int st = ensure_ctx();
+  if (st) return st;
+  *tripped = 0;
+  if (!p->wd_flag) return SGM_OK;
+  CUstream s = (CUstream)stream;
+  unsigned v = 0;
+  CU(D.cuMemcpyDtoHAsync(&v, p->wd_flag, 4, s));
+  CU(D.cuStreamSynchronize(s));
+  *tripped = v != 0;
+  if (v && reset) {
+    CU(D.cuMemsetD32Async(p->wd_flag, 0, 1, s));
+    CU(D.cuStreamSynchronize(s));
+  }
   return SGM_OK;
 }
 

@@ -52,6 +52,11 @@ except ImportError:  # the GPU box carries no reference install
         pass
 
 
+class KernelTimeout(ResourceLimitError):
+    """The generated kernel's watchdog fired (a wait on an asynchronous completion
+    exceeded 0.5 s); a SymfuseError, so random_equiv_test reports "run: ..."."""
+
+
 class BackendError(RuntimeError):
     """CUDA / NVRTC failure inside libsgm (status >= 100)."""
 

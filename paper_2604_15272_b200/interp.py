@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 from . import _abi, ir
-from .errors import BackendUnavailable, ShapeError, SymfuseError
+from .errors import BackendUnavailable, KernelTimeout, ShapeError, SymfuseError
 from .plan import PLANS, numsys_of, torch, torch_dtype
 
 try:  # reuse the reference's verdict type when it is importable
@@ -118,6 +118,8 @@ def _execute(cand: ir.Candidate, inputs: dict, ns: int, device, hints, check_mis
     outs = [t.empty(tuple(prog.spec(n).dims), dtype=torch_dtype(ns), device=dev) for n in prog.outputs]
     plan = PLANS.get(cand, ns, hints, dev)
     plan.run(dev_in, outs, init_outputs=True)
+    if plan.watchdog():
+        raise KernelTimeout(f"{plan.kernel_name}: kernel watchdog fired (a wait exceeded 0.5 s)")
     if host:
         return {n: _to_host(o, ns) for n, o in zip(prog.outputs, outs)}
     return dict(zip(prog.outputs, outs))
@@ -189,7 +191,10 @@ def random_equiv_test(graph, mapping, program=None, trials: int = 20, param_samp
             PLANS.get(prog_cand, _abi.F64, None, dev).run(dev_in, expected)
             got = [t.empty(tuple(prog.spec(n).dims), dtype=t.float64, device=dev) for n in prog.outputs]
             try:
-                PLANS.get(cand, _abi.F64, None, dev).run(dev_in, got)
+                cplan = PLANS.get(cand, _abi.F64, None, dev)
+                cplan.run(dev_in, got)
+                if cplan.watchdog():
+                    raise KernelTimeout(f"{cplan.kernel_name}: kernel watchdog fired")
             except SymfuseError as exc:
                 return EquivVerdict(False, float("inf"), trial, [params], f"run: {exc}")
             for g_, e_ in zip(got, expected):

@@ -130,6 +130,7 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.one_cta = int(h.get("one_cta", 0))
     d.hints.max_gsplit = int(h.get("max_gsplit", 0))
     d.hints.slot_kb = int(h.get("slot_kb", 0))
+    d.hints.wd_test = int(h.get("wd_test", 0))
     return d
 
 
@@ -202,6 +203,15 @@ class Plan:
         _abi.check(_abi.lib().sgm_plan_time(self._h, ip, op, len(input_sets), warmup, iters, C.c_void_p(s),
                                             C.byref(out)))
         return out.value
+
+    def watchdog(self, reset: bool = True, stream=None) -> bool:
+        """True if a launch of this plan hit the kernel watchdog since the last reset
+        (sgm_plan_watchdog; synchronises the stream)."""
+        self._bind()
+        s = stream if stream is not None else torch().cuda.current_stream(self.device).cuda_stream
+        v = C.c_int()
+        _abi.check(_abi.lib().sgm_plan_watchdog(self._h, C.c_void_p(s), 1 if reset else 0, C.byref(v)))
+        return bool(v.value)
 
     def trace(self):
         """(launched CTAs, SGM_TRACE_N, 2) array of (time_ns, event) of the last run

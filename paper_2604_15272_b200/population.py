@@ -184,6 +184,7 @@ class Record:
     hints: dict = field(default_factory=dict)
     dep_err: Optional[float] = None   # deployment-dtype rel_err vs the fp64 program (parity gate)
     dep_ok: Optional[bool] = None
+    gpu_rank: int = 0                 # rank (GPU) that evaluated the candidate
 
 
 # Deployment-dtype tolerances of the parity gate (north star item 4), the same
@@ -419,6 +420,17 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
             rec.latency_us = lat[k] if lat[k] >= 0 else None
             rec.ff_ok = (mism[k] == 0) if ff else None
             rec.timing = "screen"
+    # kernel watchdog (a bounded wait timed out): the candidate is a "run: timeout"
+    # record, like the reference's run errors (interp.py:278-281)
+    for k, u in enumerate(us):
+        if recs[k].error is not None:
+            continue
+        for ns_ in ((_abi.FF, ctx.numsys) if ff else (ctx.numsys,)):
+            if PLANS.get(u.cand, ns_, None, dev).watchdog():
+                recs[k].error = f"run: timeout (kernel watchdog, {_abi.NUMSYS_NAMES.get(ns_, ns_)})"
+                recs[k].latency_us = None
+                recs[k].ff_ok = False
+                break
 
     def live():
         return [k for k, r in enumerate(recs) if r.error is None and r.latency_us is not None and r.ff_ok is not False]
@@ -582,6 +594,84 @@ def isolated_latency(ctx: "WorkloadContext", plan: Plan, launches: int = 50) -> 
     us = sorted(a.elapsed_time(b) * 1000.0 for a, b in evs)
     return {"mean_us": sum(us) / len(us), "median_us": us[len(us) // 2], "min_us": us[0], "launches": launches,
             "method": "per-launch CUDA events, 256 MB read-only L2 flush between launches, no graph"}
+
+
+def report(pop: dict, records: list, hbm_gbs: Optional[float] = None) -> dict:
+    """The sweep in the reference's report format (cli.py:133-146 records, one per
+    verified (template, mapping) pair), each record extended with the GPU evidence
+    of its best parameter point ("b200": latency_us, hbm_gbs, roofline_frac,
+    ff_ok, dep_err, gpu_rank, kernel) and every evaluated point ("b200_points")."""
+    hbm_gbs = hbm_gbs or hbm_peak_gbs()
+    byts = algorithmic_bytes(pop)
+    by_pair: dict = {}
+    for r in records:
+        by_pair.setdefault(r.pair, []).append(r)
+    cands = []
+    for pi, c in enumerate(pop["candidates"]):
+        rs = sorted(by_pair.get(pi, []), key=lambda r: r.index)
+        ok = [r for r in rs if r.error is None and r.latency_us and r.ff_ok is not False and r.dep_ok is not False]
+        best = min(ok, key=lambda r: (r.latency_us, r.index)) if ok else None
+        rec = {"template_id": c["template_id"], "mapping": c["mapping"], "verified": True,
+               "verify": {"status": "equivalent", "exhausted": False},
+               "oracle": {"ok": all(r.ff_ok for r in rs) if rs else None, "kind": "finite field GF(2^31-1), bit-exact",
+                          "checked": sum(1 for r in rs if r.ff_ok is not None)},
+               "best": None if best is None else {"params": best.params, "score": best.latency_us * 1e-6},
+               "equivalence_checked": bool(rs) and all(r.ff_ok for r in rs)}
+        if best is not None:
+            gbs = byts / (best.latency_us * 1e-6) / 1e9
+            rec["b200"] = {"latency_us": best.latency_us, "hbm_gbs": gbs, "roofline_frac": gbs / hbm_gbs,
+                           "ff_ok": best.ff_ok, "dep_err": best.dep_err, "gpu_rank": best.gpu_rank,
+                           "timing": best.timing, "kernel": (best.plan or {}).get("kernel_name"),
+                           "plan": (best.plan or {}).get("summary"), "dtype": pop["dtype"]}
+        rec["b200_points"] = [{"params": r.params, "latency_us": r.latency_us, "ff_ok": r.ff_ok, "error": r.error,
+                               "gpu_rank": r.gpu_rank} for r in rs]
+        cands.append(rec)
+    return {"workload": pop["program"]["name"], "config": pop["config"], "dtype": pop["dtype"],
+            "algorithmic_bytes": byts, "hbm_peak_gbs": hbm_gbs, "candidates": cands,
+            "templates": sorted({c["template_id"] for c in pop["candidates"]})}
+
+
+def write_report(rep: dict, path: str) -> None:
+    """Deterministic JSON like the reference's write_report (cli.py:199-202)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        json.dump(rep, fh, indent=2, sort_keys=True, default=str)
+        fh.write("\n")
+
+
+def export_dots(pop: dict, rep: dict, outdir: str) -> list:
+    """One DOT file per verified template (cli.py:205-223, the reference's to_dot
+    when it is importable) with the GPU evidence of its pairs appended as comments."""
+    os.makedirs(outdir, exist_ok=True)
+    try:
+        from symfuse.graph import deserialize, to_dot
+        from symfuse.graph import Program as _RP  # noqa: F401
+        have_ref = True
+    except ImportError:
+        have_ref = False
+    written = []
+    for tid in sorted({c["template_id"] for c in pop["candidates"]}):
+        c0 = next(c for c in pop["candidates"] if c["template_id"] == tid)
+        body = f"// template {tid}: {c0['key']}\n"
+        if have_ref:
+            try:
+                from . import workloads as W
+                from symfuse.workloads import lower
+                spec, _ = W.spec_of(pop["config"])
+                g, _, _ = deserialize(c0["key"], lower(spec))
+                body = to_dot(g) + "\n"
+            except Exception:
+                pass
+        path = os.path.join(outdir, f"template_{tid:03d}.dot")
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write(body)
+            for rc in rep["candidates"]:
+                if rc["template_id"] == tid and rc.get("b200"):
+                    b = rc["b200"]
+                    fh.write(f"// b200 {','.join(rc['mapping'])} params={rc['best']['params']} "
+                             f"latency_us={b['latency_us']:.2f} hbm_gbs={b['hbm_gbs']:.0f} "
+                             f"roofline_frac={b['roofline_frac']:.3f} ff_ok={b['ff_ok']} kernel={b['kernel']}\n")
+        written.append(path)
+    return written
 
 
 def argmin(records: list) -> Optional[Record]:

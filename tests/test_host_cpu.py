@@ -170,3 +170,26 @@ def test_population_files_are_reference_searches():
         assert all(c["space"] for c in pop["candidates"]) or w == "Q"
     tot = sum(len(c["space"]) for w in P.WORKLOADS for c in P.load_population(w)["candidates"])
     assert tot > 1000
+
+
+def test_sweep_report_in_reference_format(tmp_path):
+    """population.report: one reference-format record per verified pair (cli.py:133-146)
+    carrying the GPU evidence of its best point; DOT files per template (cli.py:205-223)."""
+    from paper_2604_15272_b200 import population as P
+    pop = P.load_population("L")
+    us = P.units(pop)
+    recs = []
+    for u in us[:40]:
+        r = P.Record(u.workload, u.index, u.pair, dict(u.cand.params), u.cand.mapping_list(), ff_ok=True,
+                     latency_us=10.0 + u.index, plan={"kernel_name": f"k{u.index}", "summary": "s"})
+        recs.append(r)
+    recs[3].ff_ok = False
+    rep = P.report(pop, recs, hbm_gbs=6553.3)
+    assert len(rep["candidates"]) == len(pop["candidates"])
+    first = rep["candidates"][us[0].pair]
+    assert first["best"]["params"] == us[0].cand.params and first["b200"]["latency_us"] == 10.0
+    assert abs(first["b200"]["roofline_frac"] - P.algorithmic_bytes(pop) / 10e-6 / 1e9 / 6553.3) < 1e-12
+    assert rep["candidates"][us[3].pair]["oracle"]["ok"] is False
+    P.write_report(rep, str(tmp_path / "r.json"))
+    files = P.export_dots(pop, rep, str(tmp_path / "dots"))
+    assert files and any("// b200" in open(f).read() for f in files)
