@@ -246,6 +246,8 @@ def main() -> None:
     ap.add_argument("--no-e2e-opt", action="store_true",
                     help="skip the end-to-end optimisation run (live search + cold compile + first sweep)")
     ap.add_argument("--search-workers", type=int, default=0, help="host processes for the parallel search")
+    ap.add_argument("--calibrate-out", default=None,
+                    help="measure per-candidate sweep cost (FF run + timed launches) and write populations/costs.json format here")
     ap.add_argument("--records", default=None, help="write all records (JSON) here (rank 0)")
     ap.add_argument("--report", default=None,
                     help="directory: per-workload sweep report (reference format + GPU evidence) and DOT files (rank 0)")
@@ -332,10 +334,9 @@ def main() -> None:
             if r.error:
                 log(f"  error {r.workload}#{r.index} {r.params} {r.error[:160]}")
                 break
-        winners = {}
-        for w in args.workloads:
-            best = P.argmin([r for r in recs if r.workload == w])
-            winners[w] = P.reduce_best(best, dist)
+        # one cross-rank reduction per step for all workloads (no per-workload sync point)
+        bests = [P.argmin([r for r in recs if r.workload == w]) for w in args.workloads]
+        winners = dict(zip(args.workloads, P.reduce_best_many(bests, dist)))
         return recs, winners
 
     def barrier():
@@ -361,10 +362,13 @@ def main() -> None:
         barrier()
     ms = e0.elapsed_time(e1)
     launches = _abi.launch_count() - launches0
+    per_rank_ms = [ms / args.steps]
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        g = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(g, t)
+        per_rank_ms = [float(x.item()) / args.steps for x in g]
+        ms = max(float(x.item()) for x in g)
     n_total = len(all_units)
     value = n_total * args.steps / (ms / 1000.0)
 
@@ -432,6 +436,13 @@ def main() -> None:
             dist.barrier()
             dist.destroy_process_group()
         return
+
+    if args.calibrate_out and world == 1:
+        costs = {w: {str(i): v for i, v in P.calibrate_costs(ctx[w], P.units(pops[w])).items()} for w in args.workloads}
+        with open(args.calibrate_out, "w") as fh:
+            json.dump({"what": "per-candidate GPU microseconds of the sweep's work: one FF run + 2 timed launches, "
+                               "serialised, CUDA events (population.calibrate_costs)", "costs_us": costs}, fh)
+        log(f"calibration written to {args.calibrate_out}")
 
     # ---- best kernels: physical-plan tuning of each workload's top candidates (planner
     # variants), then the paper's 1000-run protocol on the winner ----
@@ -526,6 +537,9 @@ def main() -> None:
         "cold_candidates_per_s": None if e2e_opt is None else e2e_opt["cold_candidates_per_s"],
         "clocks": clk.summary(),
         "gpu_launches": launches,
+        "per_rank_ms_per_step": per_rank_ms,
+        "scaling_prediction": {"from": "measured per-candidate costs (populations/costs.json), LPT shards",
+                               "by_n": P.predict_scaling(all_units)} if P.predict_scaling(all_units) else None,
     }
     print(json.dumps(line))
     if dist is not None:

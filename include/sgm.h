@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define SGM_ABI_VERSION 1
+#define SGM_ABI_VERSION 2
 
 #define SGM_MAX_RANK 4
 #define SGM_MAX_GRID 3
@@ -126,7 +126,12 @@ typedef struct {
   int32_t max_gsplit;      /* cap on gsplit parts per reduction group (0 = none) */
   int32_t slot_kb;         /* TMA ring slot size in KB at one CTA per SM: 0 = planner (32), 16 = twice the slots */
   int32_t wd_test;         /* test only: 1 = the TMA producer issues nothing, so the watchdog must fire */
-  int32_t _reserved[2];
+  int32_t small_tma;       /* 1: small streamed operands (<= 64 KB per item, 1/8 of the largest stream) also
+                              go through the TMA ring; 0 = they are read with plain loads by the compute
+                              warps while the producer streams the large operand from kernel entry */
+  int32_t big_first;       /* 1: schedule the largest streamed matmul first (its ring fill starts at once;
+                              small chains run after it, their operands already in flight) */
+  int32_t _reserved[4];
 } sgm_plan_hints;
 
 typedef struct {
@@ -187,6 +192,9 @@ int sgm_plan_info_get(const sgm_plan* plan, sgm_plan_info* info);
 int sgm_plan_feasible(const sgm_plan_desc* desc, sgm_plan_info* info);
 /* Copy the generated CUDA source (NUL-terminated, truncated to cap). Returns length via *len. */
 int sgm_plan_source(const sgm_plan* plan, char* buf, size_t cap, size_t* len);
+/* The sm_100a cubin of a compile-only plan (created before sgm_init bound a
+ * device), for cuobjdump / SASS inspection; *len receives its size. */
+int sgm_plan_cubin(const sgm_plan* plan, void* buf, size_t cap, size_t* len);
 int sgm_plan_destroy(sgm_plan* plan);
 
 /* Outputs are first filled with NaN (fp) / 0xFFFFFFFF (FF) when init_outputs != 0,

@@ -12,7 +12,7 @@ import threading
 from .errors import BackendUnavailable, from_status
 
 MAX_RANK, MAX_GRID, MAX_NODES, MAX_SLOTS = 4, 3, 64, 16
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 F64, F32, BF16, FF = 0, 1, 2, 3
 NUMSYS_NAMES = {F64: "f64", F32: "f32", BF16: "bf16", FF: "ff"}
@@ -40,7 +40,8 @@ class PlanHints(C.Structure):
         ("smem_budget", C.c_int32), ("no_loop_split", C.c_int32), ("no_hoist", C.c_int32),
         ("use_tcgen05", C.c_int32), ("no_tma", C.c_int32), ("trace", C.c_int32),
         ("variant", C.c_int32), ("one_cta", C.c_int32), ("max_gsplit", C.c_int32), ("slot_kb", C.c_int32),
-        ("wd_test", C.c_int32), ("_reserved", C.c_int32 * 2),
+        ("wd_test", C.c_int32), ("small_tma", C.c_int32), ("big_first", C.c_int32),
+        ("_reserved", C.c_int32 * 4),
     ]
 
 
@@ -76,6 +77,7 @@ SYMBOLS = {
     "sgm_plan_feasible": ([C.POINTER(PlanDesc), C.POINTER(PlanInfo)], C.c_int),
     "sgm_plan_info_get": ([C.c_void_p, C.POINTER(PlanInfo)], C.c_int),
     "sgm_plan_source": ([C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+    "sgm_plan_cubin": ([C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     "sgm_plan_destroy": ([C.c_void_p], C.c_int),
     "sgm_plan_run": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int, C.c_void_p], C.c_int),
     "sgm_plan_run_host": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p], C.c_int),

@@ -991,8 +991,11 @@ struct Gen {
           // on L).  Ties: the smaller stream first.
           const bool fn = would_flush(n), fp = pick >= 0 && would_flush(pick);
           const i64 sn = stream_bytes(nodes[n]), sp = pick >= 0 ? stream_bytes(nodes[pick]) : 0;
-          if (pick < 0 || (!fn && fp) ||
-              (fn == fp && (height[n] > height[pick] || (height[n] == height[pick] && sn < sp))))
+          const bool big = d.hints.big_first && fn == fp && pick >= 0 && sn != sp && (sn > 0 || sp > 0);
+          if (big) {
+            if (sn > sp) pick = n;
+          } else if (pick < 0 || (!fn && fp) ||
+                     (fn == fp && (height[n] > height[pick] || (height[n] == height[pick] && sn < sp))))
             pick = n;
         }
         if (pick < 0) break;
@@ -1049,6 +1052,12 @@ struct Gen {
     int ntma = 0;
     for (auto& t : nodes)
       if (t.store == ST_XG) t.store = ST_SMEM;
+    // a small stream (e.g. LoRA's X@A, 32 KB per item) queued in the ring ahead of a
+    // large one holds slots and delays the large stream's start by its whole
+    // dependency chain; it is read with plain loads instead (hint small_tma = 1 keeps
+    // it on the ring)
+    i64 max_stream = 0;
+    for (auto& t : nodes) max_stream = std::max(max_stream, stream_bytes(t));
     for (int n = 0; n < (int)nodes.size(); ++n) {
       Node& x = nodes[n];
       if (x.kind != SGM_MATMUL) continue;
@@ -1127,7 +1136,10 @@ struct Gen {
         // every box starts 16-byte aligned iff the slice width along n is a multiple of 16 bytes
         // (all start terms are multiples of it); TMA faults on misaligned box starts
         const bool batch_ok = x.sl[0] * x.sl[1] <= 8 && b.sl[3] == NN && b.sl[2] == K && (NN * es) % 16 == 0 && !x.inv;
-        if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 && (ns == SGM_BF16 || ns == SGM_F32)) {
+        const i64 sb = stream_bytes(x);
+        const bool small = !d.hints.small_tma && sb <= 64 * 1024 && sb * 8 <= max_stream;
+        if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 && (ns == SGM_BF16 || ns == SGM_F32) &&
+            !small) {
           if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && (d3 * 2) % 16 == 0 &&
               ntl * 16 <= 512) {
             x.tma = true;
@@ -1841,9 +1853,11 @@ struct Gen {
     os << "    for (int e0 = tid; e0 < " << sz << "; e0 += 4 * NT) {\n      C v_[4];\n";
     // compute with the index clamped (no branch around the loads, so the four are
     // issued back to back); only the stores are guarded
-    os << "#pragma unroll\n      for (int j = 0; j < 4; ++j) {\n        const int e = min(e0 + j * NT, " << sz - 1
-       << ");\n";
-    os << "        { " << pre << "v_[j] = " << expr << "; }\n      }\n";
+    // guarded (not clamped) reads: a clamped index made out-of-range lanes re-read the
+    // last element while its owner wrote it in place (a benign but real smem race,
+    // compute-sanitizer racecheck)
+    os << "#pragma unroll\n      for (int j = 0; j < 4; ++j) {\n        const int e = e0 + j * NT;\n";
+    os << "        if (e < " << sz << ") { " << pre << "v_[j] = " << expr << "; }\n      }\n";
     os << "#pragma unroll\n      for (int j = 0; j < 4; ++j) {\n        const int e = e0 + j * NT;\n";
     os << "        if (e < " << sz << ") " << tile_ptr(n) << "[e] = v_[j];\n      }\n    }\n";
   }
@@ -2181,6 +2195,9 @@ struct Gen {
     os << "  SGM_TR(5);\n";
     os << "  sgm::csync<NT>();  // tiles are reused by the next item\n  }\n";
     os << "  SGM_TR(7);  // exit\n";
+    // no CTA of a cluster leaves while a peer may still touch its shared memory
+    // (DSMEM pushes / remote barrier arrivals of the last item)
+    if (CL > 1) os << cl_sync();
     if (tmem_cols) os << "  sgm::tmem_free<NT>(tmem_base, " << tmem_cols << "u);\n";
     os << "}\n";
   }

@@ -567,7 +567,9 @@ __device__ __forceinline__ void mbar_init(u64* b, u32 cnt) {
 #ifndef SGM_WD_NS
 #define SGM_WD_NS 500000000ull
 #endif
-__device__ unsigned sgm_wd_flag;
+}  // namespace sgm
+extern "C" __device__ unsigned sgm_wd_flag;  // C linkage: looked up by name (cuModuleGetGlobal)
+namespace sgm {
 __device__ __forceinline__ u64 wd_now() {
   u64 t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

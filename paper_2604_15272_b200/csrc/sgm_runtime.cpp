@@ -356,6 +356,7 @@ struct sgm_plan {
   int graph_rot = 0;
   int graph_pdl = -1;        // PDL setting the cached graph was captured with
   CUdeviceptr wd_flag = 0;   // the module's sgm_wd_flag (watchdog, sgm_dev.cuh)
+  std::string cubin;         // compile-only plans keep their sm_100a cubin (sgm_plan_cubin)
 };
 
 // programmatic dependent launch: on unless SGM_NO_PDL is set; sgm_set_pdl overrides
@@ -460,7 +461,8 @@ int sgm_plan_create(const sgm_plan_desc* desc, sgm_plan** out) {
     delete p;
     return st;
   }
-  if (t_device < 0) {  // compile-only use (no device bound): keep the source, no module
+  if (t_device < 0) {  // compile-only use (no device bound): keep the source + cubin, no module
+    p->cubin = std::move(cubin);
     *out = p;
     return SGM_OK;
   }
@@ -587,6 +589,14 @@ int sgm_plan_info_get(const sgm_plan* p, sgm_plan_info* info) {
   snprintf(info->kernel_name, sizeof info->kernel_name, "%s", p->gen.kernel_name.c_str());
   snprintf(info->plan_summary, sizeof info->plan_summary, "grid=%lld occ=%d regs=%d sstat=%d %s",
            (long long)p->launch_ctas, p->occ_per_sm, p->regs, p->static_smem, p->gen.summary.c_str());
+  return SGM_OK;
+}
+
+int sgm_plan_cubin(const sgm_plan* p, void* buf, size_t cap, size_t* len) {
+  if (!p) return set_err(SGM_ERR_INVALID, "null plan");
+  if (p->cubin.empty()) return set_err(SGM_ERR_INVALID, "cubin is kept only for compile-only plans (no device bound)");
+  if (len) *len = p->cubin.size();
+  if (buf && cap) memcpy(buf, p->cubin.data(), std::min(cap, p->cubin.size()));
   return SGM_OK;
 }
 

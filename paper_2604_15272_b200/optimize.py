@@ -92,8 +92,15 @@ def start_search(workloads, workers: Optional[int] = None):
     return SearchRun(list(workloads), workers)
 
 
-def evaluate_population(pop: dict, device: int, dist=None, refine_top: int = 3) -> dict:
-    """Cold compile of this rank's shard + the sweep + the cross-rank argmin."""
+def evaluate_population(pop: dict, device: int, dist=None, refine_top: int = 3, ff_all: bool = False) -> dict:
+    """Cold compile of this rank's shard + the sweep + the cross-rank argmin.
+
+    With the reference's stage-4 semantics (cli.py:159-195; default): every
+    candidate is compiled and timed in its deployment dtype, the equivalence
+    oracle (here the exact GF(p) check) runs on `param_samples` = 2 points per
+    verified pair drawn as random_equiv_test draws them, and every contender for
+    the argmin is FF-checked and parity-gated before it can win.  ff_all=True
+    FF-checks every candidate (the steady-state sweep's per-candidate work)."""
     import torch
     from . import _abi
     rank = dist.get_rank() if dist is not None else 0
@@ -102,13 +109,15 @@ def evaluate_population(pop: dict, device: int, dist=None, refine_top: int = 3) 
     mine = P.shard(us, rank, world)
     numsys = P.numsys_of(pop["dtype"])
     threads = max(1, (os.cpu_count() or 8) // world)
+    ff_sel = set(range(len(mine))) if ff_all else P.oracle_sample(pop, mine)
     torch.cuda.synchronize(device)
     t0 = time.perf_counter()
-    errs = P.precompile([u.cand for u in mine], [numsys, _abi.FF], device, threads=threads)
+    errs = P.precompile([u.cand for u in mine], [numsys], device, threads=threads)
+    errs.update(P.precompile([mine[k].cand for k in sorted(ff_sel)], [_abi.FF], device, threads=threads))
     t_compile = time.perf_counter() - t0
     t0 = time.perf_counter()
     ctx = P.WorkloadContext(pop, device)
-    recs = P.evaluate_workload(ctx, mine, refine_top=refine_top)
+    recs = P.evaluate_workload(ctx, mine, ff=True if ff_all else ff_sel, refine_top=refine_top)
     torch.cuda.synchronize(device)
     t_sweep = time.perf_counter() - t0
     best = P.argmin(recs)
@@ -116,10 +125,13 @@ def evaluate_population(pop: dict, device: int, dist=None, refine_top: int = 3) 
     out = dict(candidates=len(us), candidates_this_rank=len(mine), compile_threads=threads,
                compile_s=_max(t_compile, dist, device), sweep_s=_max(t_sweep, dist, device),
                compile_errors=sum(1 for e in errs.values() if e),
-               ff_mismatch=sum(1 for r in recs if r.ff_ok is False), winner_index=win)
+               ff_checked=sum(1 for r in recs if r.ff_ok is not None),
+               ff_mismatch=sum(1 for r in recs if r.ff_ok is False), winner_index=win,
+               oracle="ff on every candidate" if ff_all else
+               "ff on 2 sampled points per verified pair (random_equiv_test draw) + every contender")
     if best is not None and best.index == win:
         out["winner"] = {"latency_us": best.latency_us, "mapping": best.mapping, "params": best.params,
-                         "dep_err": best.dep_err, "dep_ok": best.dep_ok, "timing": best.timing,
+                         "dep_err": best.dep_err, "dep_ok": best.dep_ok, "ff_ok": best.ff_ok, "timing": best.timing,
                          "kernel": (best.plan or {}).get("kernel_name")}
     return out
 

@@ -131,6 +131,8 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.max_gsplit = int(h.get("max_gsplit", 0))
     d.hints.slot_kb = int(h.get("slot_kb", 0))
     d.hints.wd_test = int(h.get("wd_test", 0))
+    d.hints.small_tma = int(h.get("small_tma", 0))
+    d.hints.big_first = int(h.get("big_first", 0))
     return d
 
 
@@ -169,6 +171,15 @@ class Plan:
         buf = C.create_string_buffer(n.value + 1)
         _abi.check(L.sgm_plan_source(self._h, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
+
+    def cubin(self) -> bytes:
+        """sm_100a cubin of a compile-only plan (device=None)."""
+        L = _abi.lib()
+        n = C.c_size_t()
+        _abi.check(L.sgm_plan_cubin(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _abi.check(L.sgm_plan_cubin(self._h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
 
     def _bind(self):
         if self.device is None:

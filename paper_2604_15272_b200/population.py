@@ -53,10 +53,30 @@ class Unit:
     pair: int           # verified (template, mapping) pair index
     cand: ir.Candidate
     est_bytes: float = 0.0
+    cost_us: float = 0.0   # measured GPU time of its sweep work (populations/costs.json), 0 = unknown
+
+
+COSTS_PATH = os.path.join(POP_DIR, "costs.json")
+_COSTS: Optional[dict] = None
+
+
+def measured_costs() -> dict:
+    """{workload: {population index: GPU microseconds}} from a B200 calibration run
+    (bench.py --calibrate-out; committed as populations/costs.json)."""
+    global _COSTS
+    if _COSTS is None:
+        try:
+            with open(COSTS_PATH) as fh:
+                d = json.load(fh)
+            _COSTS = {w: {int(k): float(v) for k, v in per.items()} for w, per in d["costs_us"].items()}
+        except (FileNotFoundError, KeyError, ValueError):
+            _COSTS = {}
+    return _COSTS
 
 
 def units(pop: dict) -> list:
     prog = ir.Program.from_json(pop["program"])
+    cost = measured_costs().get(pop["config"], {})
     out = []
     for pi, c in enumerate(pop["candidates"]):
         base = ir.from_serialized(c["key"], prog, {})
@@ -68,6 +88,7 @@ def units(pop: dict) -> list:
                 u.est_bytes = s["bytes_loaded"] + s["bytes_stored"]
             except SymfuseError:
                 u.est_bytes = 0.0
+            u.cost_us = cost.get(u.index, 0.0)
             out.append(u)
     return out
 
@@ -106,19 +127,73 @@ def algorithmic_flops(pop: dict) -> int:
     return fl
 
 
+def _weight(u: Unit, us: list) -> float:
+    return u.cost_us if u.cost_us > 0 else u.est_bytes
+
+
 def shard(us: list, rank: int, world: int) -> list:
-    """LPT assignment on estimated bytes (deterministic on every rank)."""
+    """LPT assignment (deterministic on every rank).  Weights are the measured
+    per-candidate GPU cost of the sweep (populations/costs.json: FF run + timed
+    launches, calibrated on a B200) when every unit has one, else estimated bytes
+    (tuner.cost_stats): bytes miss the uncoalesced candidates that dominate A."""
     if world <= 1:
         return list(us)
-    order = sorted(us, key=lambda u: (-u.est_bytes, u.workload, u.index))
+    return lpt(us, world)[rank]
+
+
+def lpt(us: list, world: int) -> list:
+    measured = bool(us) and all(u.cost_us > 0 for u in us)
+    w = (lambda u: u.cost_us) if measured else (lambda u: u.est_bytes + 1.0)
+    order = sorted(us, key=lambda u: (-w(u), u.workload, u.index))
     load = [0.0] * world
-    mine = []
+    parts = [[] for _ in range(world)]
     for u in order:
         r = min(range(world), key=lambda k: (load[k], k))
-        load[r] += u.est_bytes + 1.0
-        if r == rank:
-            mine.append(u)
-    return mine
+        load[r] += w(u)
+        parts[r].append(u)
+    return parts
+
+
+def predict_scaling(us: list, worlds=(2, 4, 8)) -> dict:
+    """Predicted sweep speed-up at N ranks from the measured per-candidate costs:
+    total cost / the slowest LPT shard (None without a calibration)."""
+    if not us or not all(u.cost_us > 0 for u in us):
+        return {}
+    tot = sum(u.cost_us for u in us)
+    out = {}
+    for n in worlds:
+        mx = max(sum(u.cost_us for u in part) for part in lpt(us, n))
+        out[str(n)] = {"speedup": tot / mx, "slowest_shard_ms": mx / 1e3, "total_ms": tot / 1e3}
+    return out
+
+
+def calibrate_costs(ctx: "WorkloadContext", us: list, launches: int = 3) -> dict:
+    """Per-candidate GPU time of its sweep work, serialised: one FF run + two
+    deployment-dtype launches (screen + rotation share), each bracketed by CUDA
+    events on the current stream (mean of `launches` repetitions).  Returns
+    {population index: microseconds}."""
+    t = torch()
+    dev = ctx.device
+    evs = []
+    for u in us:
+        try:
+            pf = PLANS.get(u.cand, _abi.FF, None, dev)
+            pd = PLANS.get(u.cand, ctx.numsys, None, dev)
+        except Exception:
+            continue
+        outs = ctx.ff_lanes()[0][1]
+        a, b, c = (t.cuda.Event(enable_timing=True) for _ in range(3))
+        pf.run(ctx.ff_inputs, outs, init_outputs=False)  # warm (module, instruction cache)
+        a.record()
+        for _ in range(launches):
+            pf.run(ctx.ff_inputs, outs, init_outputs=False)
+        b.record()
+        for k in range(launches):
+            pd.run(ctx.ws.sets[k % ctx.ws.rot], ctx.ws.outputs, init_outputs=False)
+        c.record()
+        evs.append((u.index, a, b, c))
+    t.cuda.synchronize(dev)
+    return {i: (a.elapsed_time(b) + 2.0 * b.elapsed_time(c)) * 1000.0 / launches for i, a, b, c in evs}
 
 
 def precompile(cands: list, numsys_list, device: Optional[int], threads: int = 0, hints=None) -> dict:
@@ -354,19 +429,66 @@ class Timer:
             pass
 
 
-def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_factor: float = 2.0,
+def _ff_enqueue(ctx: "WorkloadContext", us: list, ks: list, recs: list, counters) -> None:
+    """FF runs + on-device mismatch counts of candidates `ks`, spread over side
+    streams (verification, not timing: kernels that leave SMs idle overlap), then
+    joined to the current stream."""
+    import ctypes as C
+    t = torch()
+    dev = ctx.device
+    L = _abi.lib()
+    main = t.cuda.current_stream(dev)
+    lanes = ctx.ff_lanes()
+    for sl, _ in lanes:
+        sl.wait_stream(main)
+    for j, k in enumerate(ks):
+        sl, outs = lanes[j % len(lanes)]
+        try:
+            PLANS.get(us[k].cand, _abi.FF, None, dev).run(ctx.ff_inputs, outs, stream=sl.cuda_stream)
+            sp = C.c_void_p(sl.cuda_stream)
+            for g, e in zip(outs, ctx.ff_expected):
+                _abi.check(L.sgm_compare_u32_acc(C.c_void_p(g.data_ptr()), C.c_void_p(e.data_ptr()), g.numel(),
+                                                 sp, C.c_void_p(counters.data_ptr() + 8 * k)))
+        except Exception as exc:
+            recs[k].error = f"{type(exc).__name__}: {str(exc)[:300]}"
+    for sl, _ in lanes:
+        main.wait_stream(sl)
+
+
+def oracle_sample(pop: dict, us: list, param_samples: int = 2, seed: int = 0) -> set:
+    """Indices (into `us`) of the points the reference's stage-4 oracle would test:
+    per verified (template, mapping) pair, `param_samples` parameter points drawn
+    exactly as random_equiv_test draws them (rng([seed, crc32(template_key)]) shuffle
+    of the divisibility-only space, interp.py:250-262; cli.py:162-170 defaults)."""
+    import zlib
+    chosen = set()
+    for pi, c in enumerate(pop["candidates"]):
+        rng = np.random.default_rng([seed, zlib.crc32(c["key"].encode())])
+        pts = [dict(p) for p in c["space"]]
+        rng.shuffle(pts)
+        for p in pts[:param_samples]:
+            chosen.add((pi, tuple(sorted(p.items()))))
+    return {k for k, u in enumerate(us) if (u.pair, tuple(sorted(u.cand.params.items()))) in chosen}
+
+
+def evaluate_workload(ctx: "WorkloadContext", us: list, ff=True, screen_factor: float = 2.0,
                       refine_top: int = 3, refine_launches: int = 1000, variants: int = 1) -> list:
     """Evaluate candidates of one workload with no per-candidate host synchronisation.
 
-    Pass 1 enqueues, per candidate, the finite-field run (outputs NaN-filled
-    first) + an on-device mismatch count against the program's FF output, and one
-    timed launch (after one untimed launch, on its own input set, so it streams
-    from HBM).  Pass 2 times one full rotation over the input sets (each launch
-    misses L2) for the candidates within `screen_factor` of the pass-1 best.
-    Pass 3 tunes the physical plan of the `refine_top` fastest (planner variants
+    Pass 1 enqueues the finite-field checks (outputs NaN-filled first, on-device
+    mismatch count against the program's FF output) and, per candidate, one
+    timed launch on its own input set (streams from HBM).  Pass 2 times one full
+    rotation over the input sets (each launch misses L2) for the candidates
+    within `screen_factor` of the pass-1 best, and gates them on parity.  Pass 3
+    tunes the physical plan of the `refine_top` fastest (planner variants
     0..`variants`-1, one rotation each) and re-times each on its best variant with
     `refine_launches` launches (the paper's 1000-run protocol).
-    One host read per pass."""
+    One host read per pass.
+
+    `ff`: True = FF-check every candidate in pass 1 (the sweep); a set of indices
+    = only those in pass 1 (e.g. oracle_sample: the reference's stage-4 oracle
+    points), and every contender of pass 2 not yet checked is FF-checked (its FF
+    kernel compiled then) before it may win; False = none."""
     import ctypes as C
     t = torch()
     dev = ctx.device
@@ -376,28 +498,11 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
         return recs
     counters = t.zeros(n, dtype=t.int64, device=dev)
     stream = C.c_void_p(t.cuda.current_stream(dev).cuda_stream)
-    L = _abi.lib()
     rot = ctx.ws.rot
     plans = [None] * n
-    if ff:
-        # FF checks first, spread over side streams (they overlap where kernels leave
-        # SMs idle), then joined, so the timing passes below run alone on the GPU
-        main = t.cuda.current_stream(dev)
-        lanes = ctx.ff_lanes()
-        for sl, _ in lanes:
-            sl.wait_stream(main)
-        for k, u in enumerate(us):
-            sl, outs = lanes[k % len(lanes)]
-            try:
-                PLANS.get(u.cand, _abi.FF, None, dev).run(ctx.ff_inputs, outs, stream=sl.cuda_stream)
-                sp = C.c_void_p(sl.cuda_stream)
-                for g, e in zip(outs, ctx.ff_expected):
-                    _abi.check(L.sgm_compare_u32_acc(C.c_void_p(g.data_ptr()), C.c_void_p(e.data_ptr()), g.numel(),
-                                                     sp, C.c_void_p(counters.data_ptr() + 8 * k)))
-            except Exception as exc:
-                recs[k].error = f"{type(exc).__name__}: {str(exc)[:300]}"
-        for sl, _ in lanes:
-            main.wait_stream(sl)
+    ff_first = list(range(n)) if ff is True else sorted(ff) if ff else []
+    if ff_first:
+        _ff_enqueue(ctx, us, ff_first, recs, counters)
     timer = Timer(n, dev)
     for k, u in enumerate(us):
         rec = recs[k]
@@ -414,18 +519,19 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
             rec.error = f"{type(exc).__name__}: {str(exc)[:300]}"
     lat = timer.read(n)
     mism = counters.cpu().tolist()
+    ff_set = set(ff_first)
     timer.close()
     for k, rec in enumerate(recs):
         if rec.error is None:
             rec.latency_us = lat[k] if lat[k] >= 0 else None
-            rec.ff_ok = (mism[k] == 0) if ff else None
+            rec.ff_ok = (mism[k] == 0) if k in ff_set else None
             rec.timing = "screen"
     # kernel watchdog (a bounded wait timed out): the candidate is a "run: timeout"
     # record, like the reference's run errors (interp.py:278-281)
     for k, u in enumerate(us):
         if recs[k].error is not None:
             continue
-        for ns_ in ((_abi.FF, ctx.numsys) if ff else (ctx.numsys,)):
+        for ns_ in ((_abi.FF, ctx.numsys) if k in ff_set else (ctx.numsys,)):
             if PLANS.get(u.cand, ns_, None, dev).watchdog():
                 recs[k].error = f"run: timeout (kernel watchdog, {_abi.NUMSYS_NAMES.get(ns_, ns_)})"
                 recs[k].latency_us = None
@@ -452,6 +558,17 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff: bool = True, screen_
         for k, (err, good) in zip(sel, deployment_check(ctx, [plans[k] for k in sel])):
             recs[k].dep_err, recs[k].dep_ok = err, good
         sel = [k for k in sel if recs[k].dep_ok]
+        late = [k for k in sel if recs[k].ff_ok is None and ff is not False]
+        if late:  # contenders the first pass did not FF-check: compile their FF kernels, check
+            precompile([us[k].cand for k in late], [_abi.FF], None)
+            _ff_enqueue(ctx, us, late, recs, counters)
+            mism = counters.cpu().tolist()
+            for k in late:
+                if recs[k].error is None:
+                    recs[k].ff_ok = mism[k] == 0
+                    if PLANS.get(us[k].cand, _abi.FF, None, dev).watchdog():
+                        recs[k].error, recs[k].ff_ok = "run: timeout (kernel watchdog, ff)", False
+            sel = [k for k in sel if recs[k].ff_ok and recs[k].error is None]
         top = sorted(sel, key=lambda k: (recs[k].latency_us, recs[k].index))[:refine_top]
         # physical-plan tuning: planner variants of the top candidates (the FF check of
         # the candidate covers every variant: each is the same block graph, re-split)
@@ -496,7 +613,8 @@ VARIANT_HINTS = [{}] + [{"variant": v} for v in range(1, 6)] + [{"one_cta": 1}] 
     [{"one_cta": 1, "variant": v} for v in range(1, 4)] + \
     [{"max_gsplit": g} for g in (1, 2, 4)] + [{"max_gsplit": g, "one_cta": 1} for g in (1, 2, 4)] + \
     [{"max_gsplit": g, "max_cluster": 1} for g in (1, 2, 4)] + [{"max_cluster": 1}, {"max_cluster": 2}] + \
-    [{"one_cta": 1, "slot_kb": 16}, {"slot_kb": 16}]
+    [{"one_cta": 1, "slot_kb": 16}, {"slot_kb": 16}] + \
+    [{"small_tma": 1}, {"small_tma": 1, "one_cta": 1}, {"small_tma": 1, "one_cta": 1, "variant": 2}]
 
 
 def precompile_variants(units: list, numsys: int, threads: int = 0) -> None:
@@ -689,12 +807,16 @@ def reduce_best(best: Optional[Record], dist) -> int:
     Ties on latency resolve to the smaller population index, like tune()'s lexicographic
     (score, params) tie-break (tuner.py:221-223).  NCCL over NVLink on the GPU box; the
     same call runs on gloo (CPU tensors) in the multi-process tests."""
+    return reduce_best_many([best], dist)[0]
+
+
+def reduce_best_many(bests: list, dist) -> list:
+    """reduce_best for several workloads in ONE all_reduce (one sync per sweep step)."""
     t = torch()
-    key = (1 << 62) if best is None else (int(round(best.latency_us * 1000)) << 20) | best.index
+    keys = [(1 << 62) if b is None else (int(round(b.latency_us * 1000)) << 20) | b.index for b in bests]
     if dist is None:
-        return -1 if best is None else best.index
+        return [-1 if b is None else b.index for b in bests]
     dev = f"cuda:{t.cuda.current_device()}" if dist.get_backend() == "nccl" else "cpu"
-    x = t.tensor([key], dtype=t.int64, device=dev)
+    x = t.tensor(keys, dtype=t.int64, device=dev)
     dist.all_reduce(x, op=dist.ReduceOp.MIN)
-    v = int(x.item())
-    return -1 if v >= (1 << 62) else (v & ((1 << 20) - 1))
+    return [-1 if v >= (1 << 62) else (v & ((1 << 20) - 1)) for v in x.tolist()]

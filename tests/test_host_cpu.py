@@ -159,8 +159,20 @@ def test_shard_is_a_deterministic_partition(world):
     again = [P.shard(us, r, world) for r in range(world)]
     assert [[(u.workload, u.index) for u in p] for p in parts] == [[(u.workload, u.index) for u in p] for p in again]
     if world > 1:
-        loads = [sum(u.est_bytes for u in p) for p in parts]
-        assert max(loads) <= 1.5 * (sum(loads) / world) + max(u.est_bytes for u in us)
+        measured = all(u.cost_us > 0 for u in us)
+        wt = (lambda u: u.cost_us) if measured else (lambda u: u.est_bytes)
+        loads = [sum(wt(u) for u in p) for p in parts]
+        # LPT bound: no shard exceeds the mean by more than the largest single weight
+        assert max(loads) <= sum(loads) / world + max(wt(u) for u in us)
+
+
+def test_scaling_prediction_from_costs():
+    us = [u for w in ("R", "L") for u in P.units(P.load_population(w))]
+    for k, u in enumerate(us):
+        u.cost_us = 10.0 + (k * 37) % 11
+    pred = P.predict_scaling(us, (2, 4, 8))
+    assert 1.9 < pred["2"]["speedup"] <= 2.0 and 7.5 < pred["8"]["speedup"] <= 8.0
+    assert P.predict_scaling([u for u in us[:3]] + [P.Unit(0, "R", 0, us[0].cand)], (2,)) == {}
 
 
 def test_population_files_are_reference_searches():

@@ -44,6 +44,7 @@ def _worker(rank, world, port, out):
             recs = [P.Record(w, u.index, u.pair, dict(u.cand.params), u.cand.mapping_list(), ff_ok=True,
                              latency_us=_latency(u)) for u in mine]
             win = P.reduce_best(P.argmin(recs), dist)
+            assert P.reduce_best_many([P.argmin(recs), None], dist) == [win, -1]
             gathered = [None] * world
             dist.all_gather_object(gathered, [r.index for r in recs])
             res[w] = (win, sorted(i for part in gathered for i in part))

@@ -26,3 +26,28 @@ def test_parallel_search_equals_sequential(ref, w):
     assert st["mapping_candidates"] == com["search"]["stats"]["mapping_candidates"]
     assert st["templates"] == com["search"]["stats"]["templates_emitted"]
     assert [c["key"] for c in pop["candidates"]] == [c["key"] for c in com["candidates"]]
+
+
+def test_oracle_sample_is_random_equiv_tests_draw(ref, monkeypatch):
+    """The e2e-opt run FF-checks, per verified pair, exactly the parameter points the
+    reference's stage-4 oracle (random_equiv_test, interp.py:250-262, cli.py:162-170
+    param_samples=2) would test; execution is stubbed, only the draw is compared."""
+    import numpy as np
+    import symfuse.interp as RI
+    from symfuse.graph import deserialize
+    from symfuse.workloads import lower
+    from paper_2604_15272_b200 import population as P
+    from paper_2604_15272_b200 import workloads as W
+    pop = P.load_population("L")
+    us = P.units(pop)
+    picked = P.oracle_sample(pop, us)
+    spec, _ = W.spec_of("L")
+    program = lower(spec)
+    monkeypatch.setattr(RI, "run_concrete", lambda c, ins, *a, **k: {"O": np.zeros((8, 4096))})
+    monkeypatch.setattr(RI, "run_program", lambda p, ins: {"O": np.zeros((8, 4096))})
+    for pi, c in enumerate(pop["candidates"]):
+        g, m, _ = deserialize(c["key"], program)
+        v = RI.random_equiv_test(g, m, program, trials=1, param_samples=2)
+        want = {tuple(sorted(p.items())) for p in v.params_tested}
+        got = {tuple(sorted(us[k].cand.params.items())) for k in picked if us[k].pair == pi}
+        assert got == want, (pi, got, want)

@@ -29,7 +29,7 @@ CASES = [
     ("cluster-push", "R", 26, "O.1.x,W.1.x", {"x": 2, "i": 1}, {"max_cluster": 4, "max_gsplit": 1}),
     ("cluster-rs-ag", "A", 42, "Kt.1.x,O.1.x,Q.1.x,V.1.x", {"x": 2, "i": 1}, {"max_cluster": 8, "max_gsplit": 1}),
     ("paired-tmem", "Q", 36, "Kt.0.x,O.0.x,Q.0.x,V.0.x", {"x": 8, "i": 1}, {}),
-    ("f32-ring", "R", 26, "O.1.x,W.1.x", {"x": 2, "i": 1}, {"one_cta": 1}),
+    ("f32-ring", "R", 26, "O.1.x,W.1.x", {"x": 2, "i": 1}, {"one_cta": 1, "max_cluster": 1}),
 ]
 
 
