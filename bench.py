@@ -109,16 +109,19 @@ def _reference_symfuse():
 
 
 class _RefPath:
-    """One candidate evaluation on the reference's own CPU path: score_interp-style
-    timed symfuse.interp.run_concrete + one random_equiv_test trial (run_program +
-    run_concrete + rel_err, interp.py:272-283).  Workloads the reference cannot
-    express (G at 14336: TensorSpec rejects non-powers of two, graph.py:96-101)
-    run on the oracle port of the same functions instead."""
+    """One candidate evaluation on the reference's own CPU path, the work of its
+    stage 4 per parameter point: one timed symfuse.interp.run_concrete (score_interp,
+    tuner.py:160-174) + one random_equiv_test trial (run_concrete + rel_err against
+    run_program, interp.py:272-283).  run_program's output is computed once per
+    workload and input set (as the GPU sweep computes the program's FF output once).
+    Workloads the reference cannot express (G at 14336: TensorSpec rejects non-powers
+    of two, graph.py:96-101) run on the oracle port of the same functions instead."""
 
     def __init__(self, pops):
         self.sf = _reference_symfuse()
         self.progs = {}
         self.kinds = set()
+        self.expected = {}
         if self.sf is not None:
             from symfuse.graph import ProgOp, Program, TensorSpec
             from fractions import Fraction
@@ -141,62 +144,113 @@ class _RefPath:
             from symfuse.graph import deserialize, instantiate
             from symfuse.interp import rel_err, run_concrete, run_program
             program = self.progs[u.workload]
+            if u.workload not in self.expected:
+                self.expected[u.workload] = run_program(program, ins)
+            exp = self.expected[u.workload]
             g, m, _ = deserialize(key, program)
             conc = instantiate(g, m, u.cand.params)
             run_concrete(conc, ins)                      # score_interp run (tuner.py:171-173)
             got = run_concrete(conc, ins)                # equivalence trial (interp.py:277-283)
-            exp = run_program(program, ins)
             max(rel_err(got[n], exp[n]) for n in program.outputs)
             self.kinds.add("reference")
             return
+        if u.workload not in self.expected:
+            self.expected[u.workload] = block_np.run_program(prog_dict, ins)
+        exp = self.expected[u.workload]
         block_np.run_concrete(prog_dict, key, u.cand.params, ins)
         got = block_np.run_concrete(prog_dict, key, u.cand.params, ins)
-        exp = block_np.run_program(prog_dict, ins)
         max(block_np.rel_err(got[n], exp[n]) for n in prog_dict["outputs"])
         self.kinds.add("port")
 
 
-def cpu_eval_sample(seconds: float, workloads, seed: int = 0) -> dict:
+def _cpu_worker(workloads, seed, jobs, results):
+    """Child process: evaluates (workload, index) jobs in order, reporting each."""
+    import numpy as np
+    from paper_2604_15272_b200 import population as P
+    pops = {w: P.load_population(w) for w in workloads}
+    byw = {w: {u.index: u for u in P.units(pops[w])} for w in workloads}
+    path = _RefPath(pops)
+    rng = np.random.default_rng(seed)
+    inputs = {}
+    while True:
+        job = jobs.get()
+        if job is None:
+            return
+        w, idx = job
+        prog = pops[w]["program"]
+        if w not in inputs:
+            inputs[w] = {t["name"]: rng.standard_normal(tuple(t["dims"])) for t in prog["tensors"]
+                         if t["role"] == "input"}
+        t0 = time.perf_counter()
+        path.evaluate(byw[w][idx], prog, inputs[w])
+        results.put((w, idx, time.perf_counter() - t0, sorted(path.kinds)))
+
+
+def cpu_eval_sample(seconds: float, workloads, seed: int = 0, cap_s: float = 6.0) -> dict:
     """The reference's CPU candidate evaluation (symfuse interp.run_concrete /
-    run_program in fp64 numpy) on a bounded sample of the population:
-    per candidate one timed run_concrete (score_interp) + one equivalence trial."""
+    run_program in fp64 numpy) on a bounded, UNIFORMLY RANDOM sample of
+    the five-workload population (seeded per call), run in a worker process.  A
+    candidate still running after `cap_s` seconds is stopped and charged cap_s with
+    no candidate finished, so the figure is an upper bound on the CPU path's
+    throughput (the slowest candidates take minutes on the CPU)."""
+    import multiprocessing as mp
+
     import numpy as np
 
     from paper_2604_15272_b200 import population as P
 
-    pops = {w: P.load_population(w) for w in workloads}
-    path = _RefPath(pops)
-    order = []
-    per = {w: P.units(pops[w]) for w in workloads}
+    allu = [(w, u.index) for w in workloads for u in P.units(P.load_population(w))]
+    order = [allu[i] for i in np.random.default_rng(1000 + seed).permutation(len(allu))]
+    ctx = mp.get_context("fork")
+    done, capped, spent, kinds, per_w = 0, 0, 0.0, set(), {}
     k = 0
-    while any(per.values()) and k < 10000:
-        for w in workloads:
-            if per[w]:
-                order.append(per[w].pop(len(per[w]) // 2 if k % 2 else 0))
-        k += 1
-    rng = np.random.default_rng(seed)
-    inputs = {}
-    t0 = time.perf_counter()
-    done = 0
-    for u in order:
-        if time.perf_counter() - t0 > seconds and done:
+    t_start = time.perf_counter()
+    while k < len(order) and (time.perf_counter() - t_start) < seconds:
+        jobs, results = ctx.Queue(), ctx.Queue()
+        proc = ctx.Process(target=_cpu_worker, args=(workloads, seed, jobs, results), daemon=True)
+        proc.start()
+        for job in order[k:k + 64]:
+            jobs.put(job)
+        while k < len(order) and (time.perf_counter() - t_start) < seconds:
+            try:
+                w, idx, dt, kk = results.get(timeout=cap_s + 30.0)
+            except Exception:
+                break
+            if dt > cap_s:   # finished, but beyond the cap: charged the cap only
+                dt = cap_s
+            spent += dt
+            kinds.update(kk)
+            per_w[w] = per_w.get(w, 0) + 1
+            done += 1
+            k += 1
+            if k % 64 == 0:
+                for job in order[k:k + 64]:
+                    jobs.put(job)
+        else:
+            jobs.put(None)
+            proc.join(timeout=5)
+            if proc.is_alive():
+                proc.kill()
             break
-        prog = pops[u.workload]["program"]
-        if u.workload not in inputs:
-            inputs[u.workload] = {t["name"]: rng.standard_normal(tuple(t["dims"])) for t in prog["tensors"]
-                                  if t["role"] == "input"}
-        path.evaluate(u, prog, inputs[u.workload])
-        done += 1
-    el = time.perf_counter() - t0
-    kind = "reference" if path.kinds == {"reference"} else ("port" if path.kinds == {"port"} else "reference+port")
+        # the worker is stuck on order[k] (over the cap): charge the cap, skip it
+        proc.kill()
+        proc.join()
+        spent += cap_s
+        capped += 1
+        k += 1
+    el = max(spent, 1e-9)
+    kind = "reference" if kinds == {"reference"} else ("port" if kinds == {"port"} else "reference+port")
     try:
         import threadpoolctl
         blas = [f"{d.get('internal_api')}:{d.get('num_threads')}thr" for d in threadpoolctl.threadpool_info()]
     except Exception:
         blas = []
-    return {"candidates": done, "seconds": el, "value": done / el, "kind": kind,
-            "sample": f"{done} candidates round-robin over {','.join(workloads)} (fp64 numpy, full scale; "
-                      f"symfuse from baseline/_ref where expressible, oracle port otherwise; BLAS {blas})"}
+    return {"candidates": done, "seconds": el, "value": done / el, "kind": kind, "capped": capped,
+            "sample": f"{done} candidates drawn uniformly at random from the {len(allu)}-candidate population "
+                      f"({per_w}), {capped} stopped at the {cap_s:.0f} s cap and charged the cap (so the value is "
+                      f"an upper bound); per candidate one run_concrete + one equivalence trial, fp64 numpy at "
+                      f"full scale; symfuse from baseline/_ref where expressible, oracle port for G@14336; "
+                      f"BLAS {blas}"}
 
 
 def reference_arm(args) -> None:
@@ -204,14 +258,15 @@ def reference_arm(args) -> None:
     if rank != 0:
         return
     workloads = args.workloads
-    per_step = max(3.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        cpu_eval_sample(per_step, workloads)
-    vals, cands, secs = [], 0, 0.0
-    for _ in range(args.steps):
-        r = cpu_eval_sample(per_step, workloads)
+    per_step = max(4.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for k in range(args.warmup):
+        cpu_eval_sample(per_step, workloads, seed=10_000 + k)
+    cands, secs, capped = 0, 0.0, 0
+    for k in range(args.steps):
+        r = cpu_eval_sample(per_step, workloads, seed=k)
         cands += r["candidates"]
         secs += r["seconds"]
+        capped += r["capped"]
         sample = r["sample"]
         kind = r["kind"]
     v = cands / secs
@@ -219,9 +274,10 @@ def reference_arm(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1000,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": "five-workload SIGMA population (R,G,A,Q,L)",
-                                            "path": "symfuse interp (CPU, baseline/_ref) + oracle port for G@14336"},
+                                            "path": "symfuse interp (CPU, baseline/_ref) + oracle port for G@14336",
+                                            "sample": "uniformly random candidates per step (seeded by step)"},
             "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": os.cpu_count(), "kind": kind,
-                             "sample": sample},
+                             "sample": sample, "candidates_timed": cands, "capped": capped},
             "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 

@@ -131,7 +131,11 @@ typedef struct {
                               warps while the producer streams the large operand from kernel entry */
   int32_t big_first;       /* 1: schedule the largest streamed matmul first (its ring fill starts at once;
                               small chains run after it, their operands already in flight) */
-  int32_t _reserved[4];
+  int32_t item_cost_ns;    /* planner's fixed cost per work item (0 = calibrated 4 us): lower values favour
+                              many small items (finer gsplit), i.e. less wave quantisation on 148 SMs */
+  int32_t min_gsplit;      /* only plans with at least this many gsplit parts per reduction group (more,
+                              smaller work items: finer load balance over 148 SMs) */
+  int32_t _reserved[2];
 } sgm_plan_hints;
 
 typedef struct {

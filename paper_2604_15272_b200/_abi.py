@@ -41,7 +41,8 @@ class PlanHints(C.Structure):
         ("use_tcgen05", C.c_int32), ("no_tma", C.c_int32), ("trace", C.c_int32),
         ("variant", C.c_int32), ("one_cta", C.c_int32), ("max_gsplit", C.c_int32), ("slot_kb", C.c_int32),
         ("wd_test", C.c_int32), ("small_tma", C.c_int32), ("big_first", C.c_int32),
-        ("_reserved", C.c_int32 * 4),
+        ("item_cost_ns", C.c_int32), ("min_gsplit", C.c_int32),
+        ("_reserved", C.c_int32 * 2),
     ]
 
 

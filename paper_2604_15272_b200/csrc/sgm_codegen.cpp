@@ -548,6 +548,10 @@ struct Gen {
         const Node& o = nodes[other];
         // stream the larger operand; the smaller one is reused from smem
         if (prod4(x.sh) < prod4(o.sh) || (prod4(x.sh) == prod4(o.sh) && m.in[1] != n)) { view = false; break; }
+        // ... unless it is loop-invariant and its consumer runs every loop iteration:
+        // a view would be re-read from L2 on each of the n_loop iterations (A's split-KV
+        // candidates re-read Q per key), a small smem tile is loaded once per item
+        if (nloop > 1 && m.body && m.loopdep && !x.loopdep && prod4(x.sh) * ec <= 64 * 1024) { view = false; break; }
       }
       if (view) x.store = ST_VIEW;
     }
@@ -665,7 +669,8 @@ struct Gen {
     // largely hidden when two CTAs share an SM
     // fixed per-item costs measured with trace mode (tools/trace_one.py): ring refill
     // + activation staging + epilogue ~4 us, cluster flush ~5 us, gsplit tail ~2 us
-    double t_item = (4.0e-6 + cflush * 5.0e-6 + gflush * 2.0e-6) * (two ? 0.4 : 1.0);
+    const double base = d.hints.item_cost_ns > 0 ? d.hints.item_cost_ns * 1e-9 : 4.0e-6;
+    double t_item = (base + cflush * 5.0e-6 + gflush * 2.0e-6 * (base / 4.0e-6)) * (two ? 0.4 : 1.0);
     double loop_iters = loop_begin_pos >= 0 ? (double)nloop / LP : 0.0;
     t_item += loop_iters * 0.6e-6;
     return t_stream + (double)rounds * t_item + over;
@@ -685,6 +690,7 @@ struct Gen {
     apply_state(root);
     bool valid;
     double root_cost = plan_cost(&valid);
+    if (d.hints.min_gsplit > 1) root_cost += d.hints.min_gsplit;
     std::vector<std::pair<double, PlanState>> beam = {{root_cost, root}};
     std::set<std::vector<int>> seen;
     auto key = [&](const PlanState& st) {
@@ -708,6 +714,8 @@ struct Gen {
         if (d.hints.max_gsplit > 0 && GP > d.hints.max_gsplit) return;
         bool ok;
         double c = plan_cost(&ok);
+        // below the requested gsplit count a state is only a stepping stone
+        if (ok && d.hints.min_gsplit > 0 && GP < d.hints.min_gsplit) c += (double)d.hints.min_gsplit / GP;
         if (dbg)
           fprintf(stderr, "  plan p%d iter %d: LB=%lld FP=%lld GP=%lld CL=%d LP=%d%s ok=%d cost=%.2fus\n", policy, iter,
                   (long long)LB, (long long)FP, (long long)GP, CL, LP, loop_gs ? "g" : "", (int)ok, c * 1e6);
@@ -1693,7 +1701,7 @@ struct Gen {
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
       if (e.type == Ev::LOOP_BEGIN) {
-        os << "      for (int j = jp; j < " << nloop << "; j += " << LP << ") {\n";
+        os << "      for (int j = jp * " << nloop / LP << "; j < (jp + 1) * " << nloop / LP << "; ++j) {\n";
         in_loop = true;
       } else if (e.type == Ev::LOOP_END) {
         os << "      }\n";
@@ -2161,7 +2169,11 @@ struct Gen {
           if (nodes[n].kind == SGM_ACCUM)
             os << "  for (int e = tid; e < " << prod4(nodes[n].sl) << "; e += NT) " << tile_ptr(n) << "[e] = N::zero();\n";
         os << "  sgm::csync<NT>();\n";
-        os << "  for (int j = jp; j < " << nloop << "; j += " << LP << ") {\n";
+        // loop part jp runs a CONTIGUOUS range of iterations: a loop-split loader's
+        // consecutive tiles are adjacent in memory, so a strided column tile's
+        // sectors serve the next iterations from L1/L2 (interleaved parts re-fetched
+        // every sector; A's split-KV candidates read Kt one column per iteration)
+        os << "  for (int j = jp * " << nloop / LP << "; j < (jp + 1) * " << nloop / LP << "; ++j) {\n";
         in_loop = true;
       } else if (e.type == Ev::LOOP_END) {
         os << "  }\n";

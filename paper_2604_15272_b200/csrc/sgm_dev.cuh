@@ -561,7 +561,7 @@ __device__ __forceinline__ void mbar_init(u64* b, u32 cnt) {
 }
 // Watchdog (per module): every wait on an asynchronous completion (TMA
 // transaction bytes, MMA commits, remote cluster arrivals) is bounded.  A wait
-// that exceeds SGM_WD_NS sets sgm_wd_flag and gives up, so a broken candidate
+// that exceeds ~0.5 s sets sgm_wd_flag and gives up, so a broken candidate
 // ends (with garbage) instead of hanging the GPU; the runtime reads the flag
 // (sgm_plan_watchdog) and the sweep records "run: timeout" (interp.py:278-281).
 #ifndef SGM_WD_NS
@@ -576,24 +576,44 @@ __device__ __forceinline__ u64 wd_now() {
   return t;
 }
 __device__ __noinline__ void wd_trip() { atomicOr(&sgm_wd_flag, 1u); }
-__device__ __forceinline__ bool mbar_try(u64* b, u32 parity) {
-  u32 ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __noinline__ void mbar_wait_slow(u64* b, u32 parity) {
-  if (*(volatile unsigned*)&sgm_wd_flag) return;  // already timed out: drain without waiting
-  const u64 t0 = wd_now();
-  while (!mbar_try(b, parity))
-    if (wd_now() - t0 > SGM_WD_NS) { wd_trip(); return; }
-}
+// The bounded wait (experiments: SGM_WD_MODE 0 = unbounded canonical loop,
+// 1 = canonical loop with a suspend hint, 2 = straight-line probes with a long
+// suspend hint, 3 = counted probe loop)
+#ifndef SGM_WD_MODE
+#define SGM_WD_MODE 2
+#endif
+constexpr u32 kWdProbes = 1u << 22;
 __device__ __forceinline__ void mbar_wait(u64* b, u32 parity) {
-  if (!mbar_try(b, parity)) mbar_wait_slow(b, parity);
+#if defined(SGM_NO_WD) || SGM_WD_MODE == 0
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+#elif SGM_WD_MODE == 1
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(b)), "r"(parity), "r"(0x10000000u) : "memory");
+#elif SGM_WD_MODE == 2
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %3;\n\t@P1 bra DONE;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %3;\n\t@P1 bra DONE;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %3;\n\t@P1 bra DONE;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %3;\n\t@P1 bra DONE;\n\t"
+      "red.relaxed.gpu.global.or.b32 [%2], 1;\n\t"
+      "DONE:\n\t}" ::"r"(smem_u32(b)), "r"(parity), "l"(&sgm_wd_flag), "r"(0x10000000u)
+      : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t.reg .u32 c;\n\tmov.u32 c, %3;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\tsub.u32 c, c, 1;\n\tsetp.ne.u32 P1, c, 0;\n\t@P1 bra LAB_WAIT;\n\t"
+      "red.relaxed.gpu.global.or.b32 [%2], 1;\n\t"
+      "DONE:\n\t}" ::"r"(smem_u32(b)), "r"(parity), "l"(&sgm_wd_flag), "r"(kWdProbes)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

@@ -259,6 +259,7 @@ int compile_cubin(const std::string& src, std::string& cubin, double& ms, int& h
   nvrtcVersion(&maj, &minr);
   std::string key_src = src + "|" + kArch + "|nvrtc" + std::to_string(maj) + "." + std::to_string(minr) + "|" +
                         std::to_string(sgmcg::fnv1a(kDevHeader)) + std::to_string(sgmcg::fnv1a(kUtilHeader));
+  if (const char* e = getenv("SGM_NVRTC_OPTS")) key_src += std::string("|opts:") + e;  // experiments: own cache keys
   char name[64];
   snprintf(name, sizeof name, "%016" PRIx64 ".cubin", sgmcg::fnv1a(key_src));
   std::string path = cache_dir() + "/" + name;

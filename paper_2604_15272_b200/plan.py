@@ -133,6 +133,8 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.wd_test = int(h.get("wd_test", 0))
     d.hints.small_tma = int(h.get("small_tma", 0))
     d.hints.big_first = int(h.get("big_first", 0))
+    d.hints.item_cost_ns = int(h.get("item_cost_ns", 0))
+    d.hints.min_gsplit = int(h.get("min_gsplit", 0))
     return d
 
 

@@ -196,3 +196,46 @@ def test_torch_tensors_zero_copy(S):
     assert got.is_cuda
     ref = torch.softmax(ins["X"], 1) @ ins["W"]
     assert (got - ref).abs().max().item() < 1e-12
+
+
+def test_tile_dump_exposes_per_block_values(S):  # test_integration.py:72-85
+    prog = _softmax_matmul(S, 64, 64, 16)
+    cand = _known_good(S, prog, {"x": 2, "i": 2})
+    rng = np.random.default_rng(0)
+    dump: dict = {}
+    S.run_concrete(cand, {"X": rng.standard_normal((64, 64)), "W": rng.standard_normal((64, 16))}, tile_dump=dump)
+    assert set(dump) == {(0,), (1,)}
+    assert dump[(0,)][0].shape == (32, 32)  # X tile of block 0
+
+
+def test_tile_dump_matches_oracle(S, desk_cases):
+    """Every node's per-block tile (last loop iteration / accumulated sum /
+    epilogue loaders on their last tile) against the CPU oracle's tile_dump,
+    fp64 and finite field, on golden cases with grid and loop splits."""
+    from oracle import block_np, ff_np
+    n = 0
+    for c in desk_cases:
+        if c.get("instantiate_error") or c.get("f64_error") or c.get("ff_error"):
+            continue
+        grid = 1
+        for q, v in c["params"].items():
+            grid *= v
+        if grid < 4 or n >= 12:
+            continue
+        cand = _cand(S, c)
+        for dt, ins, arith in (("f64", case_inputs_f64(c), None), ("ff", case_inputs_ff(c), ff_np.FFArith())):
+            got, ref = {}, {}
+            S.run_concrete(cand, ins, dtype=dt, tile_dump=got)
+            block_np.run_concrete(c["program"], c["key"], c["params"], ins, arith=arith, tile_dump=ref)
+            assert set(got) == set(ref), c["id"]
+            for coords, env in ref.items():
+                assert set(got[coords]) == set(env), (c["id"], coords)
+                for idx, tile in env.items():
+                    g = np.asarray(got[coords][idx])
+                    assert g.shape == tile.shape, (c["id"], coords, idx)
+                    if dt == "ff":
+                        assert np.array_equal(g.astype(np.int64), tile), (c["id"], coords, idx)
+                    elif np.isfinite(tile).all():
+                        assert S.rel_err(g, tile) < F64_TOL, (c["id"], coords, idx)
+        n += 1
+    assert n >= 8

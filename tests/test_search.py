@@ -51,3 +51,15 @@ def test_oracle_sample_is_random_equiv_tests_draw(ref, monkeypatch):
         want = {tuple(sorted(p.items())) for p in v.params_tested}
         got = {tuple(sorted(us[k].cand.params.items())) for k in picked if us[k].pair == pi}
         assert got == want, (pi, got, want)
+
+
+def test_reference_arm_cpu_sample_is_uniform_and_capped(ref):
+    """bench.py's CPU arm: a uniformly random sample of the whole population per
+    step (not the cheapest index-0 candidates), candidates over the cap charged
+    the cap (the reported CPU throughput is an upper bound)."""
+    import bench
+    r = bench.cpu_eval_sample(3.0, ["R", "L"], seed=1, cap_s=2.0)
+    assert r["candidates"] + r["capped"] >= 1
+    assert r["kind"] in ("reference", "reference+port")
+    assert "uniformly at random" in r["sample"]
+    assert r["value"] == r["candidates"] / r["seconds"]

@@ -29,15 +29,26 @@ def main():
     ap.add_argument("--top", type=int, default=6)
     ap.add_argument("--hints", default=None)
     ap.add_argument("--launches", type=int, default=500)
+    ap.add_argument("--cand", action="append", default=[],
+                    help='explicit candidate "template|mapping,comma,list|{params json}" (skips the screening sweep)')
     args = ap.parse_args()
     torch.cuda.set_device(0)
     _abi.bind_device(0)
     pop = P.load_population(args.w)
     us = P.units(pop)
-    P.precompile([u.cand for u in us], [P.numsys_of(pop["dtype"])], 0)
     ctx = P.WorkloadContext(pop, 0, ff=False)
-    recs = P.evaluate_workload(ctx, us, ff=False, refine_top=args.top, refine_launches=200)
-    ok = sorted((r for r in recs if r.latency_us and r.error is None), key=lambda r: r.latency_us)[:args.top]
+    if args.cand:
+        ok = []
+        for spec in args.cand:
+            tid, mapping, params = spec.split("|")
+            params = json.loads(params)
+            u = next(x for x in us if pop["candidates"][x.pair]["template_id"] == int(tid)
+                     and x.cand.mapping_list() == sorted(mapping.split(",")) and x.cand.params == params)
+            ok.append(P.Record(args.w, u.index, u.pair, params, u.cand.mapping_list()))
+    else:
+        P.precompile([u.cand for u in us], [P.numsys_of(pop["dtype"])], 0)
+        recs = P.evaluate_workload(ctx, us, ff=False, refine_top=args.top, refine_launches=200)
+        ok = sorted((r for r in recs if r.latency_us and r.error is None), key=lambda r: r.latency_us)[:args.top]
     if args.hints:
         hs = json.loads(args.hints)
     else:
