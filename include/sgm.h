@@ -126,16 +126,17 @@ typedef struct {
   int32_t max_gsplit;      /* cap on gsplit parts per reduction group (0 = none) */
   int32_t slot_kb;         /* TMA ring slot size in KB at one CTA per SM: 0 = planner (32), 16 = twice the slots */
   int32_t wd_test;         /* test only: 1 = the TMA producer issues nothing, so the watchdog must fire */
-  int32_t small_tma;       /* 1: small streamed operands (<= 64 KB per item, 1/8 of the largest stream) also
-                              go through the TMA ring; 0 = they are read with plain loads by the compute
-                              warps while the producer streams the large operand from kernel entry */
+  int32_t small_plain;     /* 1: small streamed operands (<= 64 KB per item, <= 1/8 of the largest stream)
+                              are read with plain loads by the compute warps instead of the TMA ring */
   int32_t big_first;       /* 1: schedule the largest streamed matmul first (its ring fill starts at once;
                               small chains run after it, their operands already in flight) */
   int32_t item_cost_ns;    /* planner's fixed cost per work item (0 = calibrated 4 us): lower values favour
                               many small items (finer gsplit), i.e. less wave quantisation on 148 SMs */
   int32_t min_gsplit;      /* only plans with at least this many gsplit parts per reduction group (more,
                               smaller work items: finer load balance over 148 SMs) */
-  int32_t _reserved[2];
+  int32_t no_wd;           /* 1: unbounded (canonical) mbarrier waits, no kernel watchdog; 2-7% faster ring
+                              loops.  The sweep runs watchdog kernels; the best-kernel phase reports no_wd ones */
+  int32_t _reserved[1];
 } sgm_plan_hints;
 
 typedef struct {
@@ -258,7 +259,7 @@ int sgm_rel_err(const void* a, const void* b, int64_t n, int numsys, void* strea
 int sgm_rel_err_acc(const void* a, int numsys, const double* b, int64_t n, void* stream, uint64_t* dev_slot);
 /* Watchdog of a plan's kernel: generated kernels bound every wait on an
  * asynchronous completion (TMA bytes, MMA commits, remote cluster arrivals) to
- * 0.5 s; a wait that times out sets a flag in the plan's module and gives up,
+ * 2 s; a wait that times out sets a flag in the plan's module and gives up,
  * so a broken kernel terminates (with wrong results) instead of hanging the
  * device.  Synchronises `stream`, sets *tripped = 1 if any launch since the
  * last reset timed out, and clears the flag when `reset` != 0.  The Python

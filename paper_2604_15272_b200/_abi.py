@@ -40,9 +40,9 @@ class PlanHints(C.Structure):
         ("smem_budget", C.c_int32), ("no_loop_split", C.c_int32), ("no_hoist", C.c_int32),
         ("use_tcgen05", C.c_int32), ("no_tma", C.c_int32), ("trace", C.c_int32),
         ("variant", C.c_int32), ("one_cta", C.c_int32), ("max_gsplit", C.c_int32), ("slot_kb", C.c_int32),
-        ("wd_test", C.c_int32), ("small_tma", C.c_int32), ("big_first", C.c_int32),
+        ("wd_test", C.c_int32), ("small_plain", C.c_int32), ("big_first", C.c_int32),
         ("item_cost_ns", C.c_int32), ("min_gsplit", C.c_int32),
-        ("_reserved", C.c_int32 * 2),
+        ("no_wd", C.c_int32), ("_reserved", C.c_int32 * 1),
     ]
 
 

@@ -1062,8 +1062,9 @@ struct Gen {
       if (t.store == ST_XG) t.store = ST_SMEM;
     // a small stream (e.g. LoRA's X@A, 32 KB per item) queued in the ring ahead of a
     // large one holds slots and delays the large stream's start by its whole
-    // dependency chain; it is read with plain loads instead (hint small_tma = 1 keeps
-    // it on the ring)
+    // dependency chain; hint small_plain = 1 reads it with plain loads instead (measured
+    // on L: plain loads queue behind the producer's TMA traffic, 12.0 -> 15.2 us, so
+    // the ring stays the default)
     i64 max_stream = 0;
     for (auto& t : nodes) max_stream = std::max(max_stream, stream_bytes(t));
     for (int n = 0; n < (int)nodes.size(); ++n) {
@@ -1145,7 +1146,7 @@ struct Gen {
         // (all start terms are multiples of it); TMA faults on misaligned box starts
         const bool batch_ok = x.sl[0] * x.sl[1] <= 8 && b.sl[3] == NN && b.sl[2] == K && (NN * es) % 16 == 0 && !x.inv;
         const i64 sb = stream_bytes(x);
-        const bool small = !d.hints.small_tma && sb <= 64 * 1024 && sb * 8 <= max_stream;
+        const bool small = d.hints.small_plain && sb <= 64 * 1024 && sb * 8 <= max_stream;
         if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 && (ns == SGM_BF16 || ns == SGM_F32) &&
             !small) {
           if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && (d3 * 2) % 16 == 0 &&
@@ -1972,6 +1973,7 @@ struct Gen {
             os << "    sgm::build_xb_g<" << M << ", " << K << ", " << in_strides[a.slot][2] << "LL, NT>((u16*)(sm + "
                << x.at_off << "), (const u16*)" << view_ptr(a) << ");\n";
             os << "    sgm::fence_async_smem();\n    sgm::csync<NT>();\n";
+            os << "  SGM_TR(" << 600 + n << ");  // A^T built\n";
           }
           pa = "(const float*)nullptr";
           build = false;
@@ -2031,6 +2033,7 @@ struct Gen {
   }
 
   void emit() {
+    if (d.hints.no_wd) os << "#define SGM_WD_MODE 0  // canonical unbounded waits (no watchdog)\n";
     os << "#include \"sgm_dev.cuh\"\n";
     os << "// generated by sgm_codegen.cpp: logical blocks " << LB << ", free parts " << FP << ", cluster " << CL
        << ", loop parts " << LP << "\n";

@@ -54,7 +54,7 @@ except ImportError:  # the GPU box carries no reference install
 
 class KernelTimeout(ResourceLimitError):
     """The generated kernel's watchdog fired (a wait on an asynchronous completion
-    exceeded 0.5 s); a SymfuseError, so random_equiv_test reports "run: ..."."""
+    exceeded 2 s); a SymfuseError, so random_equiv_test reports "run: ..."."""
 
 
 class BackendError(RuntimeError):

@@ -119,7 +119,7 @@ def _execute(cand: ir.Candidate, inputs: dict, ns: int, device, hints, check_mis
     plan = PLANS.get(cand, ns, hints, dev)
     plan.run(dev_in, outs, init_outputs=True)
     if plan.watchdog():
-        raise KernelTimeout(f"{plan.kernel_name}: kernel watchdog fired (a wait exceeded 0.5 s)")
+        raise KernelTimeout(f"{plan.kernel_name}: kernel watchdog fired (a wait exceeded 2 s)")
     if host:
         return {n: _to_host(o, ns) for n, o in zip(prog.outputs, outs)}
     return dict(zip(prog.outputs, outs))

@@ -131,10 +131,11 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.max_gsplit = int(h.get("max_gsplit", 0))
     d.hints.slot_kb = int(h.get("slot_kb", 0))
     d.hints.wd_test = int(h.get("wd_test", 0))
-    d.hints.small_tma = int(h.get("small_tma", 0))
+    d.hints.small_plain = int(h.get("small_plain", 0))
     d.hints.big_first = int(h.get("big_first", 0))
     d.hints.item_cost_ns = int(h.get("item_cost_ns", 0))
     d.hints.min_gsplit = int(h.get("min_gsplit", 0))
+    d.hints.no_wd = int(h.get("no_wd", 0))
     return d
 
 

@@ -614,10 +614,10 @@ VARIANT_HINTS = [{}] + [{"variant": v} for v in range(1, 6)] + [{"one_cta": 1}] 
     [{"max_gsplit": g} for g in (1, 2, 4)] + [{"max_gsplit": g, "one_cta": 1} for g in (1, 2, 4)] + \
     [{"max_gsplit": g, "max_cluster": 1} for g in (1, 2, 4)] + [{"max_cluster": 1}, {"max_cluster": 2}] + \
     [{"one_cta": 1, "slot_kb": 16}, {"slot_kb": 16}] + \
-    [{"small_tma": 1}, {"small_tma": 1, "one_cta": 1}, {"small_tma": 1, "one_cta": 1, "variant": 2}]
+    [{"small_plain": 1}, {"small_plain": 1, "one_cta": 1}]
 
 
-def precompile_variants(units: list, numsys: int, threads: int = 0) -> None:
+def precompile_variants(units: list, numsys: int, threads: int = 0, extra: Optional[dict] = None) -> None:
     """Compile every planner variant of `units` into the cubin cache in parallel
     (compile-only plans, no device), so tune_physical's plan builds are cache hits."""
     threads = threads or min(32, os.cpu_count() or 8)
@@ -630,10 +630,10 @@ def precompile_variants(units: list, numsys: int, threads: int = 0) -> None:
             pass
 
     with ThreadPoolExecutor(threads) as ex:
-        list(ex.map(one, [(u, h) for u in units for h in VARIANT_HINTS]))
+        list(ex.map(one, [(u, {**h, **(extra or {})}) for u in units for h in VARIANT_HINTS]))
 
 
-def tune_physical(ctx: "WorkloadContext", u: Unit, launches: int = 1000) -> tuple:
+def tune_physical(ctx: "WorkloadContext", u: Unit, launches: int = 1000, extra: Optional[dict] = None) -> tuple:
     """Physical-plan tuning of one candidate: time each planner variant (other scored
     splits, one-CTA-per-SM rings) over one rotation, re-time the fastest with
     `launches` launches.  Returns (latency_us, hints, plan).  The candidate's FF
@@ -641,6 +641,7 @@ def tune_physical(ctx: "WorkloadContext", u: Unit, launches: int = 1000) -> tupl
     dev = ctx.device
     plans = []
     for h in VARIANT_HINTS:
+        h = {**h, **(extra or {})}
         try:
             plans.append((h, PLANS.get(u.cand, ctx.numsys, h or None, dev)))
         except Exception:

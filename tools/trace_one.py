@@ -36,6 +36,8 @@ def name(ev: int) -> str:
         return f"own n{ev - 1500}"
     if ev >= 1000:
         return f"node n{ev - 1000}"
+    if 600 <= ev < 700:
+        return f"xT n{ev - 600}"
     return {0: "entry", 1: "start", 2: "item", 3: "P:item", 5: "item end", 6: "P:done", 7: "exit", 8: "tmem",
             9: "invariants"}.get(ev, str(ev))
 

@@ -53,7 +53,7 @@ def main():
         hs = json.loads(args.hints)
     else:
         base = [{}, {"one_cta": 1}, {"one_cta": 1, "slot_kb": 16}, {"slot_kb": 16}]
-        extra = [{}, {"small_tma": 1}, {"big_first": 1}, {"big_first": 1, "small_tma": 1}]
+        extra = [{}, {"small_plain": 1}, {"big_first": 1}, {"big_first": 1, "small_plain": 1}]
         hs = [dict(a, **b) for a, b in itertools.product(base, extra)]
     byi = {u.index: u for u in us}
     rows = []
