@@ -335,11 +335,20 @@ def main() -> None:
     if not args.no_e2e_opt and rank == 0:
         from paper_2604_15272_b200 import optimize
         search_run = optimize.start_search(args.workloads, args.search_workers or None)
+    # test mode for the N>1 host logic on a 1-GPU box: every rank on GPU 0, gloo
+    # (NCCL refuses two ranks per GPU); the driver's multi-GPU runs use NCCL
+    if os.environ.get("SGM_ONE_GPU"):
+        local = 0
+    backend = os.environ.get("SGM_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = f"cuda:{local}" if backend == "nccl" else "cpu"
     _abi.bind_device(local)
 
     e2e_opt = None
@@ -380,7 +389,8 @@ def main() -> None:
         t_w = {}
         for w in args.workloads:
             t0 = time.perf_counter()
-            recs.extend(P.evaluate_workload(ctx[w], mine_by_w[w], refine_top=args.refine_top))
+            recs.extend(P.evaluate_workload(ctx[w], mine_by_w[w], refine_top=args.refine_top,
+                                            select=P.global_top(dist, args.refine_top) if dist is not None else None))
             t_w[w] = time.perf_counter() - t0
         errs = sum(1 for r in recs if r.error)
         log("step " + " ".join(f"{w}:{t:.2f}s" for w, t in t_w.items()) + f" errors={errs}")
@@ -420,7 +430,7 @@ def main() -> None:
     launches = _abi.launch_count() - launches0
     per_rank_ms = [ms / args.steps]
     if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([ms], dtype=torch.float64, device=coll_dev)
         g = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(g, t)
         per_rank_ms = [float(x.item()) / args.steps for x in g]
@@ -464,7 +474,8 @@ def main() -> None:
                 for dst, src in zip(c.ff_inputs + c.ws.sets[0], host[w]):
                     dst.copy_(src, non_blocking=True)
                 c.refresh_expected()  # the program's own FF run on the freshly copied inputs
-                rs = P.evaluate_workload(c, mine_by_w[w], refine_top=args.refine_top)
+                rs = P.evaluate_workload(c, mine_by_w[w], refine_top=args.refine_top,
+                                         select=P.global_top(dist, args.refine_top) if dist is not None else None)
                 d2h += 16 * len(rs)  # mismatch counters + latencies
         e2e_step()
         torch.cuda.synchronize()
@@ -478,7 +489,7 @@ def main() -> None:
         ems = f0.elapsed_time(f1)
         log(f"e2e: {ems:.0f} ms/step, h2d {h2d / 1e9:.2f} GB")
         if dist is not None:
-            t = torch.tensor([ems, h2d, d2h], dtype=torch.float64, device=f"cuda:{local}")
+            t = torch.tensor([ems, h2d, d2h], dtype=torch.float64, device=coll_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t[0].item())
             h2d, d2h = int(t[1].item()) * world, int(t[2].item()) * world
@@ -496,8 +507,9 @@ def main() -> None:
     if args.calibrate_out and world == 1:
         costs = {w: {str(i): v for i, v in P.calibrate_costs(ctx[w], P.units(pops[w])).items()} for w in args.workloads}
         with open(args.calibrate_out, "w") as fh:
-            json.dump({"what": "per-candidate GPU microseconds of the sweep's work: one FF run + 2 timed launches, "
-                               "serialised, CUDA events (population.calibrate_costs)", "costs_us": costs}, fh)
+            json.dump({"what": "per-candidate GPU microseconds of the sweep's work (cost_us: one FF run + 2 timed "
+                               "launches, serialised; dep_us: one deployment-dtype launch), CUDA events "
+                               "(population.calibrate_costs)", "costs_us": costs}, fh)
         log(f"calibration written to {args.calibrate_out}")
 
     # ---- best kernels: physical-plan tuning of each workload's top candidates (planner

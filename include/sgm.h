@@ -136,7 +136,10 @@ typedef struct {
                               smaller work items: finer load balance over 148 SMs) */
   int32_t no_wd;           /* 1: unbounded (canonical) mbarrier waits, no kernel watchdog; 2-7% faster ring
                               loops.  The sweep runs watchdog kernels; the best-kernel phase reports no_wd ones */
-  int32_t _reserved[1];
+  int32_t interleave;      /* 1: issue the first ring-full of the largest tcgen05 stream before a small
+                              independent stream chain scheduled ahead of it (LoRA's X@A -> T@B), the
+                              rest after it: the chain runs while the ring refills */
+  int32_t _reserved[3];
 } sgm_plan_hints;
 
 typedef struct {

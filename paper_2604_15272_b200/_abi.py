@@ -42,7 +42,8 @@ class PlanHints(C.Structure):
         ("variant", C.c_int32), ("one_cta", C.c_int32), ("max_gsplit", C.c_int32), ("slot_kb", C.c_int32),
         ("wd_test", C.c_int32), ("small_plain", C.c_int32), ("big_first", C.c_int32),
         ("item_cost_ns", C.c_int32), ("min_gsplit", C.c_int32),
-        ("no_wd", C.c_int32), ("_reserved", C.c_int32 * 1),
+        ("no_wd", C.c_int32), ("interleave", C.c_int32),
+        ("_reserved", C.c_int32 * 3),
     ]
 
 

@@ -179,6 +179,12 @@ struct Gen {
   double est_us = 0;     // planner's time estimate
   int ringS = 0;
   int ring_off = 0;
+  // interleave: the big stream `ilv_big` issues k-chunks [0, ilv_kc) before the small
+  // chain that starts at schedule position ilv_pos, the rest at its own position;
+  // chain MMAs use TMEM columns from ilv_tmem (after the big stream's accumulators)
+  int ilv_big = -1, ilv_pos = -1, ilv_kc = 0, ilv_tmem = 0;
+  std::set<int> ilv_chain;
+  bool emit_seg1 = false;  // emit_node(ilv_big) emits the first segment (build + MMAs only)
   static constexpr int kSlot = 32768;  // largest ring slot; plan_ring may pick 16 KB
   int slotB = 32768;
   static constexpr int kSmemCap = 225 * 1024;  // dynamic smem incl. ring alignment slack
@@ -1635,7 +1641,7 @@ struct Gen {
   }
 
   // producer-side stage sequence of one streamed matmul (mirrors mm_stream_tc / mm_stream_f32)
-  void emit_producer_node(int n, bool in_loop) {
+  void emit_producer_node(int n, bool in_loop, int kb = 0, int ke = -1) {
     const Node& x = nodes[n];
     const Node& a = nodes[x.in[0]];
     const Node& b = nodes[x.in[1]];
@@ -1650,7 +1656,8 @@ struct Gen {
        << ", d3 = c3 + " << (b.sl[0] > 1 ? "bi / " + std::to_string(x.sl[1]) : std::string("0")) << ";\n";
     if (x.tc) {
       i64 ntl = (NN + 127) / 128;
-      os << "          for (int kc = 0; kc < " << K / x.kc << "; ++kc)\n";
+      if (ke < 0) ke = (int)(K / x.kc);
+      os << "          for (int kc = " << kb << "; kc < " << ke << "; ++kc)\n";
       os << "            for (int t = 0; t < " << ntl << "; ++t) {\n";
       os << "              const unsigned slot = sgm::ring_acquire<" << ringS << ">(empty, pq++);\n";
       os << "              const int nb = (" << NN << " - t * 128 > 64) ? 2 : 1;\n";
@@ -1707,8 +1714,10 @@ struct Gen {
       } else if (e.type == Ev::LOOP_END) {
         os << "      }\n";
         in_loop = false;
-      } else if (e.type == Ev::NODE && nodes[e.node].kind == SGM_MATMUL && nodes[e.node].tma) {
-        emit_producer_node(e.node, in_loop);
+      } else if (e.type == Ev::NODE) {
+        if (p == ilv_pos) emit_producer_node(ilv_big, in_loop, 0, ilv_kc);
+        if (nodes[e.node].kind == SGM_MATMUL && nodes[e.node].tma)
+          emit_producer_node(e.node, in_loop, e.node == ilv_big ? ilv_kc : 0);
       }
     }
     os << "      }\n      SGM_TRP(6);\n    }\n    return;\n";
@@ -1968,8 +1977,11 @@ struct Gen {
         std::string pa = a.store == ST_VIEW ? view_ptr(a) : tile_ptr(x.in[0]);
         std::string pb = b.store == ST_VIEW ? view_ptr(b) : tile_ptr(x.in[1]);
         bool build = x.xb_build;
+        const bool chain_node = ilv_big >= 0 && ilv_chain.count(n);
+        const bool prebuilt = chain_node && x.in[0] == nodes[ilv_big].in[0] && x.at_off == nodes[ilv_big].at_off;
         if (x.tma && x.tc && a.store == ST_XG) {
-          if (x.xb_build) {
+          const bool big_build = n == ilv_big ? emit_seg1 : x.xb_build;
+          if (big_build && !prebuilt) {
             os << "    sgm::build_xb_g<" << M << ", " << K << ", " << in_strides[a.slot][2] << "LL, NT>((u16*)(sm + "
                << x.at_off << "), (const u16*)" << view_ptr(a) << ");\n";
             os << "    sgm::fence_async_smem();\n    sgm::csync<NT>();\n";
@@ -1979,10 +1991,16 @@ struct Gen {
           build = false;
         }
         if (x.tma && x.tc) {
+          // interleaved big stream: its first ilv_kc k-chunks were issued before the chain
+          const std::string seg =
+              n != ilv_big ? std::string()
+                           : emit_seg1 ? ", 0, " + std::to_string(ilv_kc) + ", false"
+                                       : ", " + std::to_string(ilv_kc) + ", " + std::to_string(K / x.kc) + ", true";
+          const std::string tm = chain_node ? "tmem_base + " + std::to_string(ilv_tmem) + "u" : std::string("tmem_base");
           os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS << ", "
-             << slotB << ", NT, " << (build ? "true" : "false") << ", " << x.acc << ">(" << tile_ptr(n) << ", " << pa << ", sm + " << x.at_off
-             << ", tmem_base, ring, full, empty, done, sq, sdph);\n";
+             << slotB << ", NT, " << (build ? "true" : "false") << ", " << x.acc << seg << ">(" << tile_ptr(n) << ", " << pa
+             << ", sm + " << x.at_off << ", " << tm << ", ring, full, empty, done, sq, sdph);\n";
         } else if (x.tma) {
           os << "    sgm::mm_stream_f32<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << x.bw << ", "
@@ -2121,6 +2139,12 @@ struct Gen {
     int tmem_cols = 0;
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) tmem_cols = std::max(tmem_cols, x.tc_cols);
+    if (ilv_big >= 0) {  // big-stream accumulators + the chain's, side by side
+      int c = 0;
+      for (int n : ilv_chain) c = std::max(c, nodes[n].tc_cols);
+      tmem_cols = 32;
+      while (tmem_cols < ilv_tmem + c) tmem_cols *= 2;
+    }
     if (tmem_cols) {
       os << "  __shared__ unsigned tmem_slot;\n";
       os << "  const unsigned tmem_base = sgm::tmem_alloc<NT>(&tmem_slot, " << tmem_cols << "u);\n";
@@ -2189,6 +2213,12 @@ struct Gen {
         emit_gflush(e.flush, p);
         gs_open = true;
       } else if (!nodes[e.node].inv) {
+        if (p == ilv_pos) {  // the big stream's first ring-full, ahead of the small chain
+          os << "  SGM_TR(" << 1700 + ilv_big << ");\n";
+          emit_seg1 = true;
+          emit_node(ilv_big, in_loop);
+          emit_seg1 = false;
+        }
         if (nodes[e.node].kind == SGM_MATMUL || nodes[e.node].kind == SGM_SUM) os << "  SGM_TR(" << 1000 + e.node << ");\n";
         if (d.hints.trace) {  // thread 0's own share done (before the node's closing barrier)
           std::ostringstream keep;
@@ -2217,6 +2247,69 @@ struct Gen {
     os << "}\n";
   }
 
+  // ---- interleave (hint, one CTA per SM): see the members.  Measured on L
+  // (x=2/8/32): 12.5-13.1 us against 12.0 us in the schedule order -- with W's
+  // boxes first, the X^T build's plain loads queue behind the TMA burst (2.5 us
+  // instead of 1.0 us).  Kept as an opt-in physical variant.  Legal when the big stream is a
+  // single-batch tcgen05 TMA matmul outside the loop whose A operand is built
+  // straight from global bf16 (ST_XG), the nodes scheduled right before it are
+  // tcgen05 TMA matmuls it does not consume (and views), and none of their
+  // shared-memory regions overlaps the big stream's A^T buffer.
+  void plan_interleave() {
+    ilv_big = ilv_pos = -1;
+    ilv_chain.clear();
+    if (!d.hints.interleave || !prod || paired) return;
+    int big = -1;
+    i64 best = 0;
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      const Node& x = nodes[n];
+      if (x.kind == SGM_MATMUL && x.tma && x.tc && stream_bytes(x) > best) { best = stream_bytes(x); big = n; }
+    }
+    if (big < 0) return;
+    const Node& B = nodes[big];
+    const Node& BA = nodes[B.in[0]];
+    if (B.body || B.inv || B.sl[0] * B.sl[1] != 1 || BA.store != ST_XG) return;
+    int pb = -1;
+    for (int p = 0; p < (int)sched.size(); ++p)
+      if (sched[p].type == Ev::NODE && sched[p].node == big) pb = p;
+    if (pb < 0) return;
+    int ps = pb;
+    std::set<int> chain;
+    for (int p = pb - 1; p >= 0; --p) {
+      const Ev& e = sched[p];
+      if (e.type != Ev::NODE) break;
+      const Node& y = nodes[e.node];
+      if (y.kind == SGM_INPUT && y.store == ST_VIEW) { ps = p; continue; }
+      if (y.kind != SGM_MATMUL || !y.tma || !y.tc || y.inv || y.body || y.sl[0] * y.sl[1] != 1) break;
+      if (B.in[0] == e.node || B.in[1] == e.node) break;
+      chain.insert(e.node);
+      ps = p;
+    }
+    if (chain.empty()) return;
+    const i64 K = BA.sl[3];
+    const int nkc = (int)(K / B.kc), ntl = (int)((B.sl[3] + 127) / 128);
+    if (nkc < 2 || ringS / ntl < 1) return;
+    // shared-memory hazards: the big stream's A^T buffer must survive the chain
+    const i64 xb0 = B.at_off, xb1 = B.at_off + 32 * K;
+    auto overlaps = [&](i64 a0, i64 a1) { return a0 < xb1 && xb0 < a1; };
+    for (int c : chain) {
+      const Node& y = nodes[c];
+      const bool same_xb = y.in[0] == B.in[0] && y.at_off == B.at_off;
+      if (!same_xb && y.at_bytes && overlaps(y.at_off, y.at_off + y.at_bytes)) return;
+      if (y.store == ST_SMEM && overlaps(y.off, y.off + prod4(y.sl) * ec)) return;
+    }
+    int cols = 0;
+    for (int c : chain) cols = std::max(cols, nodes[c].tc_cols);
+    int total = 32;
+    while (total < B.tc_cols + cols) total *= 2;
+    if (total > (paired ? 256 : 512)) return;  // two CTAs per SM share the 512 TMEM columns
+    ilv_big = big;
+    ilv_pos = ps;
+    ilv_chain = chain;
+    ilv_kc = std::max(1, std::min(nkc - 1, ringS / ntl));
+    ilv_tmem = B.tc_cols;
+  }
+
   GenResult run() {
     if (!load() || !shapes()) return R;
     structure();
@@ -2228,6 +2321,7 @@ struct Gen {
       ok = fit();
     }
     plan_ring();
+    plan_interleave();
     if (d.hints.trace) {
       trace_off = scratch_per_cta;
       scratch_per_cta += SGM_TRACE_N * 16;

@@ -951,13 +951,19 @@ __device__ __forceinline__ void build_xb_g(u16* __restrict__ xb, const u16* __re
 // only ~8 issue cycles, so a long K chain of a single 128-column tile (attention's
 // P@V) is latency-bound; consecutive MMAs rotate over the accumulators instead
 // and the epilogue adds them.
+// KB..KE: the k-chunk range this call consumes (a big stream may be split in two
+// segments with a small, dependent chain issued in between, see sgm_codegen.cpp
+// interleave); FIN = false issues the segment's MMAs only (accumulators stay in
+// TMEM, no commit to `done`, no read-back).
 template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int SLOT, int NT,
-          bool BUILD = true, int ACC = 1>
+          bool BUILD = true, int ACC = 1, int KB = 0, int KE = K / KC, bool FIN = true>
 __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const float* __restrict__ A,
                                                unsigned char* __restrict__ xbuf, u32 tmem, unsigned char* ring,
                                                u64* full, u64* empty, u64* done, u32 q, u32 dph) {
   constexpr int NTL = (NN + 127) / 128;
-  constexpr int NKC = K / KC;
+  constexpr int NKC = KE - KB;
+  static_assert(KB == 0 && KE == K / KC && FIN || (B0 * B1 == 1 && !BUILD && 0 <= KB && KB < KE && KE <= K / KC),
+                "segmented stream: one batch, prebuilt A^T");
   constexpr bool SPLIT = M <= 8;
   constexpr u32 IDESC = UMMA_IDESC_BF16_M128_N16;
   constexpr int NMMA = K / 16;                      // MMAs per tile
@@ -984,10 +990,10 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
     if (tid == 0) {
       const u32 xs = smem_u32(xb);
 #pragma unroll 1
-      for (int kc = 0; kc < NKC; ++kc) {
+      for (int kc = KB; kc < KE; ++kc) {
 #pragma unroll 1
         for (int t = 0; t < NTL; ++t) {
-          const u32 slot = ring_wait<S>(full, q0 + (u32)(kc * NTL + t));
+          const u32 slot = ring_wait<S>(full, q0 + (u32)((kc - KB) * NTL + t));
           tc_fence_after();
           const u32 st = smem_u32(ring + slot * SLOT);
 #pragma unroll
@@ -1000,8 +1006,9 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
           umma_commit(&empty[slot]);
         }
       }
-      umma_commit(done);
+      if constexpr (FIN) umma_commit(done);
     }
+    if constexpr (!FIN) return;
     mbar_wait(done, dph);
     dph ^= 1u;
     tc_fence_after();
@@ -1030,14 +1037,14 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
 // Out of line (one copy per shape): a kernel's later calls of the same shape run
 // from a warm instruction cache; the ring/phase counters advance deterministically.
 template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int SLOT, int NT,
-          bool BUILD = true, int ACC = 1>
+          bool BUILD = true, int ACC = 1, int KB = 0, int KE = K / KC, bool FIN = true>
 __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const float* __restrict__ A,
                                              unsigned char* __restrict__ xbuf, u32 tmem, unsigned char* ring, u64* full,
                                              u64* empty, u64* done, u32& q, u32& dph) {
-  mm_stream_tc_core<B0, B1, M, K, NN, SA0, SA1, SA2, SA3, KC, S, SLOT, NT, BUILD, ACC>(out, A, xbuf, tmem, ring, full,
-                                                                                      empty, done, q, dph);
-  q += (u32)(B0 * B1 * (K / KC) * ((NN + 127) / 128));
-  dph ^= (u32)((B0 * B1) & 1);
+  mm_stream_tc_core<B0, B1, M, K, NN, SA0, SA1, SA2, SA3, KC, S, SLOT, NT, BUILD, ACC, KB, KE, FIN>(
+      out, A, xbuf, tmem, ring, full, empty, done, q, dph);
+  q += (u32)(B0 * B1 * (KE - KB) * ((NN + 127) / 128));
+  if constexpr (FIN) dph ^= (u32)((B0 * B1) & 1);
 }
 
 // Streamed fp32 contraction on CUDA cores.  Stage (t, kc) = one TMA box

@@ -117,7 +117,8 @@ def evaluate_population(pop: dict, device: int, dist=None, refine_top: int = 3, 
     t_compile = time.perf_counter() - t0
     t0 = time.perf_counter()
     ctx = P.WorkloadContext(pop, device)
-    recs = P.evaluate_workload(ctx, mine, ff=True if ff_all else ff_sel, refine_top=refine_top)
+    recs = P.evaluate_workload(ctx, mine, ff=True if ff_all else ff_sel, refine_top=refine_top,
+                               select=P.global_top(dist, refine_top) if dist is not None else None)
     torch.cuda.synchronize(device)
     t_sweep = time.perf_counter() - t0
     best = P.argmin(recs)

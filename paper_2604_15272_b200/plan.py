@@ -136,6 +136,7 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.item_cost_ns = int(h.get("item_cost_ns", 0))
     d.hints.min_gsplit = int(h.get("min_gsplit", 0))
     d.hints.no_wd = int(h.get("no_wd", 0))
+    d.hints.interleave = int(h.get("interleave", 0))
     return d
 
 

@@ -54,6 +54,7 @@ class Unit:
     cand: ir.Candidate
     est_bytes: float = 0.0
     cost_us: float = 0.0   # measured GPU time of its sweep work (populations/costs.json), 0 = unknown
+    dep_us: float = 0.0    # measured deployment-kernel launch time (populations/costs.json), 0 = unknown
 
 
 COSTS_PATH = os.path.join(POP_DIR, "costs.json")
@@ -68,7 +69,9 @@ def measured_costs() -> dict:
         try:
             with open(COSTS_PATH) as fh:
                 d = json.load(fh)
-            _COSTS = {w: {int(k): float(v) for k, v in per.items()} for w, per in d["costs_us"].items()}
+            _COSTS = {w: {int(k): (float(v["cost_us"]) if isinstance(v, dict) else float(v),
+                                   float(v.get("dep_us", 0.0)) if isinstance(v, dict) else 0.0)
+                          for k, v in per.items()} for w, per in d["costs_us"].items()}
         except (FileNotFoundError, KeyError, ValueError):
             _COSTS = {}
     return _COSTS
@@ -88,7 +91,7 @@ def units(pop: dict) -> list:
                 u.est_bytes = s["bytes_loaded"] + s["bytes_stored"]
             except SymfuseError:
                 u.est_bytes = 0.0
-            u.cost_us = cost.get(u.index, 0.0)
+            u.cost_us, u.dep_us = cost.get(u.index, (0.0, 0.0))
             out.append(u)
     return out
 
@@ -154,16 +157,29 @@ def lpt(us: list, world: int) -> list:
     return parts
 
 
-def predict_scaling(us: list, worlds=(2, 4, 8)) -> dict:
+def predict_scaling(us: list, worlds=(2, 4, 8), refine_top: int = 3, refine_launches: int = 1000) -> dict:
     """Predicted sweep speed-up at N ranks from the measured per-candidate costs:
-    total cost / the slowest LPT shard (None without a calibration)."""
+    LPT shards of the per-candidate work, plus the 1000-launch refine of each
+    workload's global top `refine_top` charged to the rank that owns it
+    (evaluate_workload(select=global_top)); speed-up = (total work) / (slowest
+    rank).  Empty without a calibration."""
     if not us or not all(u.cost_us > 0 for u in us):
         return {}
-    tot = sum(u.cost_us for u in us)
+    refine = {}
+    if all(u.dep_us > 0 for u in us):
+        byw: dict = {}
+        for u in us:
+            byw.setdefault(u.workload, []).append(u)
+        for w, uu in byw.items():
+            for u in sorted(uu, key=lambda x: (x.dep_us, x.index))[:refine_top]:
+                refine[(u.workload, u.index)] = u.dep_us * refine_launches
+    tot = sum(u.cost_us for u in us) + sum(refine.values())
     out = {}
     for n in worlds:
-        mx = max(sum(u.cost_us for u in part) for part in lpt(us, n))
-        out[str(n)] = {"speedup": tot / mx, "slowest_shard_ms": mx / 1e3, "total_ms": tot / 1e3}
+        loads = [sum(u.cost_us + refine.get((u.workload, u.index), 0.0) for u in part) for part in lpt(us, n)]
+        mx = max(loads)
+        out[str(n)] = {"speedup": tot / mx, "slowest_rank_ms": mx / 1e3, "total_ms": tot / 1e3,
+                       "refine_ms": sum(refine.values()) / 1e3}
     return out
 
 
@@ -171,7 +187,7 @@ def calibrate_costs(ctx: "WorkloadContext", us: list, launches: int = 3) -> dict
     """Per-candidate GPU time of its sweep work, serialised: one FF run + two
     deployment-dtype launches (screen + rotation share), each bracketed by CUDA
     events on the current stream (mean of `launches` repetitions).  Returns
-    {population index: microseconds}."""
+    {population index: {"cost_us": ..., "dep_us": one deployment launch}}."""
     t = torch()
     dev = ctx.device
     evs = []
@@ -193,7 +209,8 @@ def calibrate_costs(ctx: "WorkloadContext", us: list, launches: int = 3) -> dict
         c.record()
         evs.append((u.index, a, b, c))
     t.cuda.synchronize(dev)
-    return {i: (a.elapsed_time(b) + 2.0 * b.elapsed_time(c)) * 1000.0 / launches for i, a, b, c in evs}
+    return {i: {"cost_us": (a.elapsed_time(b) + 2.0 * b.elapsed_time(c)) * 1000.0 / launches,
+                "dep_us": b.elapsed_time(c) * 1000.0 / launches} for i, a, b, c in evs}
 
 
 def precompile(cands: list, numsys_list, device: Optional[int], threads: int = 0, hints=None) -> dict:
@@ -472,7 +489,7 @@ def oracle_sample(pop: dict, us: list, param_samples: int = 2, seed: int = 0) ->
 
 
 def evaluate_workload(ctx: "WorkloadContext", us: list, ff=True, screen_factor: float = 2.0,
-                      refine_top: int = 3, refine_launches: int = 1000, variants: int = 1) -> list:
+                      refine_top: int = 3, refine_launches: int = 1000, variants: int = 1, select=None) -> list:
     """Evaluate candidates of one workload with no per-candidate host synchronisation.
 
     Pass 1 enqueues the finite-field checks (outputs NaN-filled first, on-device
@@ -485,6 +502,10 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff=True, screen_factor: 
     `refine_launches` launches (the paper's 1000-run protocol).
     One host read per pass.
 
+    `select`: sharded sweeps pass global_top(dist, k): every rank offers its local
+    top `refine_top` and refines only those among the global top `refine_top`, so
+    the 1000-launch refine costs k per workload, not k per rank.
+
     `ff`: True = FF-check every candidate in pass 1 (the sweep); a set of indices
     = only those in pass 1 (e.g. oracle_sample: the reference's stage-4 oracle
     points), and every contender of pass 2 not yet checked is FF-checked (its FF
@@ -495,6 +516,8 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff=True, screen_factor: 
     n = len(us)
     recs = [Record(u.workload, u.index, u.pair, dict(u.cand.params), u.cand.mapping_list()) for u in us]
     if n == 0:
+        if select is not None:
+            select([])  # collective: every rank takes part
         return recs
     counters = t.zeros(n, dtype=t.int64, device=dev)
     stream = C.c_void_p(t.cuda.current_stream(dev).cuda_stream)
@@ -542,6 +565,8 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff=True, screen_factor: 
         return [k for k, r in enumerate(recs) if r.error is None and r.latency_us is not None and r.ff_ok is not False]
 
     ok = live()
+    if not ok and select is not None:
+        select([])  # collective: every rank takes part
     if ok:
         best = min(recs[k].latency_us for k in ok)
         sel = [k for k in ok if recs[k].latency_us <= screen_factor * best]
@@ -570,6 +595,9 @@ def evaluate_workload(ctx: "WorkloadContext", us: list, ff=True, screen_factor: 
                         recs[k].error, recs[k].ff_ok = "run: timeout (kernel watchdog, ff)", False
             sel = [k for k in sel if recs[k].ff_ok and recs[k].error is None]
         top = sorted(sel, key=lambda k: (recs[k].latency_us, recs[k].index))[:refine_top]
+        if select is not None:  # sharded sweep: only this rank's share of the GLOBAL top candidates
+            keep = select([(recs[k].latency_us, recs[k].index) for k in top])
+            top = [k for k in top if recs[k].index in keep]
         # physical-plan tuning: planner variants of the top candidates (the FF check of
         # the candidate covers every variant: each is the same block graph, re-split)
         best_plan = {k: (recs[k].latency_us, 0, plans[k]) for k in top}
@@ -663,6 +691,19 @@ def tune_physical(ctx: "WorkloadContext", u: Unit, launches: int = 1000, extra: 
     best = timer.read(1)[0]
     timer.close()
     return best, h, p
+
+
+def global_top(dist, k: int):
+    """select= callback of evaluate_workload for a sharded sweep: all_gather every
+    rank's local (latency, index) contenders and keep the global k fastest (ties
+    to the smaller index).  Every rank must call it the same number of times."""
+    def select(local: list) -> set:
+        if dist is None:
+            return {i for _, i in sorted(local)[:k]}
+        parts = [None] * dist.get_world_size()
+        dist.all_gather_object(parts, list(local))
+        return {i for _, i in sorted(x for p in parts for x in p)[:k]}
+    return select
 
 
 def ff_check_plan(ctx: "WorkloadContext", cand: ir.Candidate, hints: Optional[dict]) -> bool:

@@ -151,3 +151,27 @@ def test_physical_plan_variants_deployment_dtype(S, w, template, mapping, params
     for name in prog["outputs"]:
         assert S.rel_err(got[name], exp[name]) < TOL[dt], (w, hints)
         assert np.array_equal(np.asarray(got[name]), np.asarray(got2[name])), (w, hints)
+
+
+@pytest.mark.parametrize("params", [{"x": 32, "i": 1}, {"x": 2, "i": 1}, {"x": 8, "i": 1}])
+@pytest.mark.parametrize("hints", [{"interleave": 1, "one_cta": 1}, {"interleave": 1, "one_cta": 1, "no_wd": 1},
+                                   {"interleave": 1, "one_cta": 1, "slot_kb": 16}])
+def test_interleaved_stream_deployment_dtype(S, params, hints):
+    """LoRA with the big stream (X@W) split around the small chain (X@A -> T@B):
+    first ring-full of W issued ahead of the chain, chain MMAs in their own TMEM
+    columns, the rest of W after it; bf16 against the fp64 oracle, twice (ring
+    and TMEM state carried across launches)."""
+    from oracle import block_np
+    from paper_2604_15272_b200 import population as P
+    pop = P.load_population("L")
+    u = next(x for x in P.units(pop) if x.cand.mapping_list() == ["B.1.x", "O.1.x", "W.1.x"]
+             and x.cand.params == params and pop["candidates"][x.pair]["template_id"] == 4)
+    assert ", false>(t" in S.Plan(u.cand, 2, hints, None).source()  # the stream really is segmented
+    rng = np.random.default_rng(23)
+    prog = pop["program"]
+    ins = {t["name"]: _round(rng.standard_normal(tuple(t["dims"])), "bf16") for t in prog["tensors"]
+           if t["role"] == "input"}
+    exp = block_np.run_program(prog, ins)
+    for _ in range(2):
+        got = S.run_concrete(u.cand, ins, dtype="bf16", hints=hints)
+        assert S.rel_err(got["O"], exp["O"]) < TOL["bf16"], (params, hints)

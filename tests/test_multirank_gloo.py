@@ -47,7 +47,9 @@ def _worker(rank, world, port, out):
             assert P.reduce_best_many([P.argmin(recs), None], dist) == [win, -1]
             gathered = [None] * world
             dist.all_gather_object(gathered, [r.index for r in recs])
-            res[w] = (win, sorted(i for part in gathered for i in part))
+            local = sorted((r.latency_us, r.index) for r in recs)[:3]
+            top = P.global_top(dist, 3)(local)   # the sharded refine selection (evaluate_workload select=)
+            res[w] = (win, sorted(i for part in gathered for i in part), sorted(top))
         out[rank] = res
     finally:
         dist.destroy_process_group()
@@ -64,7 +66,9 @@ def test_sharded_argmin_matches_single_process(world):
     for w in ("R", "L"):
         us = P.units(P.load_population(w))
         expect = min(us, key=lambda u: (round(_latency(u) * 1000), u.index)).index
+        top3 = sorted(u.index for u in sorted(us, key=lambda u: (_latency(u), u.index))[:3])
         for r in range(world):
-            win, idx = out[r][w]
+            win, idx, top = out[r][w]
             assert win == expect, (w, r)
             assert idx == sorted(u.index for u in us)
+            assert top == top3, (w, r)

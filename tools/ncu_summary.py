@@ -2,6 +2,10 @@
 
   python tools/ncu_summary.py <tag> gpurun_out/prof_G.ncu-rep [...]   -> profiles/<tag>_ncu.json + .md
   python tools/ncu_summary.py <tag> --launches gpurun_out/launches_G.csv
+  python tools/ncu_summary.py <tag> --traffic best.json gpurun_out/prof_*.ncu-rep
+      -> also merges DRAM bytes per launch of every captured kernel into
+         profiles/ncu_traffic.json {"kernels": {name: {...}}} (bench.py reads it
+         for roofline.traffic of the kernel it reports, and only that kernel)
 
 For each --set full report: duration, DRAM bytes read/written (per launch),
 DRAM throughput %, tensor-pipe %, warps active %, registers, grid/block, and
@@ -88,7 +92,29 @@ def launches(path: str) -> dict:
 def main(argv):
     tag = argv[0]
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    if argv[1] == "--launches":
+    if argv[1] == "--traffic":
+        best = json.load(open(argv[2]))
+        res = {os.path.basename(p): raw(p) for p in argv[3:]}
+        path = os.path.join(ROOT, "profiles", f"{tag}_ncu.json")
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        try:
+            traffic = json.load(open(tpath))
+        except Exception:
+            traffic = {}
+        kern = traffic.get("kernels", {}) if isinstance(traffic.get("kernels"), dict) else {}
+        by_kernel = {b["kernel"]: w for w, b in best.items() if "kernel" in b}
+        for rep, rows in res.items():
+            for r in rows:
+                w = by_kernel.get(r["kernel"])
+                kern[r["kernel"]] = {"workload": w, "dram_bytes": r.get("dram_read", 0) + r.get("dram_write", 0),
+                                     "dram_read": r.get("dram_read"), "dram_write": r.get("dram_write"),
+                                     "duration_us_ncu": r.get("duration"), "dram_pct": r.get("dram_pct"),
+                                     "algorithmic_bytes": best[w]["algorithmic_bytes"] if w else None,
+                                     "source": f"profiles/{tag}_ncu.json ({rep}, ncu --set full)"}
+        with open(tpath, "w") as fh:
+            json.dump({"what": "DRAM bytes (read + write) per launch of captured kernels, keyed by kernel name",
+                       "kernels": kern}, fh, indent=1)
+    elif argv[1] == "--launches":
         res = {os.path.basename(p): launches(p) for p in argv[2:]}
         path = os.path.join(ROOT, "profiles", f"{tag}_launches.json")
     else:
