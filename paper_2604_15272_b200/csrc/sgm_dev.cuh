@@ -277,11 +277,29 @@ __device__ __forceinline__ void load_tile(typename N::C* __restrict__ dst, const
       }
     }
   } else {
-    for (int e = threadIdx.x; e < ROWS * D3; e += NT) {
-      const int i3 = e % D3;
-      const int r = e / D3;
-      const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
-      dst[e] = N::ld(src[i0 * S0 + i1 * S1 + i2 * S2 + (i64)i3 * S3]);
+    // scalar (strided / unaligned) tiles: batches of 8 independent loads in flight
+    // per thread too (a column tile of A's split-KV loop is 2048 strided elements
+    // per iteration; one load at a time made each iteration ~8 round trips long)
+    constexpr int TOT = ROWS * D3;
+    constexpr int IT = (TOT + NT - 1) / NT;
+    constexpr int BT = IT < 8 ? IT : 8;
+    for (int b = 0; b < IT; b += BT) {
+      S u[BT];
+#pragma unroll
+      for (int j = 0; j < BT; ++j) {
+        const int e = threadIdx.x + (b + j) * NT;
+        if (b + j < IT && e < TOT) {
+          const int i3 = e % D3;
+          const int r = e / D3;
+          const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
+          u[j] = src[i0 * S0 + i1 * S1 + i2 * S2 + (i64)i3 * S3];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < BT; ++j) {
+        const int e = threadIdx.x + (b + j) * NT;
+        if (b + j < IT && e < TOT) dst[e] = N::ld(u[j]);
+      }
     }
   }
 }
