@@ -397,7 +397,13 @@ __device__ __forceinline__ void mm_generic(typename N::C* __restrict__ out, cons
   constexpr int OUT = B0 * B1 * M * NN;
   constexpr int TPO0 = pow2_floor(NT / OUT > 0 ? NT / OUT : 1);
   constexpr int TPO1 = TPO0 > 32 ? 32 : TPO0;
-  constexpr int TPO = TPO1 > pow2_ceil(K) ? pow2_ceil(K) : TPO1;
+  // dot-product form (both operands contiguous along k): a whole warp per output,
+  // lanes on consecutive k -- conflict-free shared-memory reads.  With few lanes per
+  // output, lanes of different rows hit one bank (row stride a multiple of 32
+  // words): A's Q @ Kt-column step took 12.7 us per loop iteration.
+  constexpr bool DOT = SA3 == 1 && SB2 == 1 && K >= 32;
+  constexpr int TPO2 = DOT ? 32 : TPO1;
+  constexpr int TPO = TPO2 > pow2_ceil(K) ? pow2_ceil(K) : TPO2;
   constexpr int GROUPS = NT / TPO;
   const int tid = threadIdx.x, lane = tid & 31;
   const u32 gmask = (TPO == 32) ? 0xffffffffu : (((1u << TPO) - 1u) << (lane & ~(TPO - 1)));
