@@ -186,57 +186,66 @@ def _cpu_worker(workloads, seed, jobs, results):
         results.put((w, idx, time.perf_counter() - t0, sorted(path.kinds)))
 
 
+_CPU_WORKER: dict = {}
+
+
+def _cpu_worker_get(workloads, seed: int):
+    """The persistent CPU worker (inputs generated once per workload and kept)."""
+    import multiprocessing as mp
+    w = _CPU_WORKER.get("w")
+    if w is not None and w["proc"].is_alive() and w["workloads"] == list(workloads):
+        return w
+    _cpu_worker_kill()
+    ctx = mp.get_context("fork")
+    jobs, results = ctx.Queue(), ctx.Queue()
+    proc = ctx.Process(target=_cpu_worker, args=(list(workloads), seed, jobs, results), daemon=True)
+    proc.start()
+    _CPU_WORKER["w"] = {"proc": proc, "jobs": jobs, "results": results, "workloads": list(workloads)}
+    return _CPU_WORKER["w"]
+
+
+def _cpu_worker_kill():
+    w = _CPU_WORKER.pop("w", None)
+    if w is not None and w["proc"].is_alive():
+        w["proc"].kill()
+        w["proc"].join()
+
+
 def cpu_eval_sample(seconds: float, workloads, seed: int = 0, cap_s: float = 6.0) -> dict:
     """The reference's CPU candidate evaluation (symfuse interp.run_concrete /
     run_program in fp64 numpy) on a bounded, UNIFORMLY RANDOM sample of
-    the five-workload population (seeded per call), run in a worker process.  A
-    candidate still running after `cap_s` seconds is stopped and charged cap_s with
-    no candidate finished, so the figure is an upper bound on the CPU path's
+    the five-workload population (seeded per call), run in a persistent worker
+    process (inputs generated once).  A candidate still running after `cap_s`
+    seconds is stopped (the worker is restarted) and charged cap_s with no
+    candidate finished, so the figure is an upper bound on the CPU path's
     throughput (the slowest candidates take minutes on the CPU)."""
-    import multiprocessing as mp
-
     import numpy as np
 
     from paper_2604_15272_b200 import population as P
 
     allu = [(w, u.index) for w in workloads for u in P.units(P.load_population(w))]
     order = [allu[i] for i in np.random.default_rng(1000 + seed).permutation(len(allu))]
-    ctx = mp.get_context("fork")
     done, capped, spent, kinds, per_w = 0, 0, 0.0, set(), {}
     k = 0
     t_start = time.perf_counter()
     while k < len(order) and (time.perf_counter() - t_start) < seconds:
-        jobs, results = ctx.Queue(), ctx.Queue()
-        proc = ctx.Process(target=_cpu_worker, args=(workloads, seed, jobs, results), daemon=True)
-        proc.start()
-        for job in order[k:k + 64]:
-            jobs.put(job)
-        while k < len(order) and (time.perf_counter() - t_start) < seconds:
-            try:
-                w, idx, dt, kk = results.get(timeout=cap_s + 30.0)
-            except Exception:
-                break
-            if dt > cap_s:   # finished, but beyond the cap: charged the cap only
-                dt = cap_s
-            spent += dt
-            kinds.update(kk)
-            per_w[w] = per_w.get(w, 0) + 1
-            done += 1
+        wk = _cpu_worker_get(workloads, 0)
+        wk["jobs"].put(order[k])
+        try:
+            w, idx, dt, kk = wk["results"].get(timeout=cap_s + 60.0)  # + first-use input generation
+        except Exception:
+            # stuck on order[k] beyond the cap: charge the cap, restart the worker
+            _cpu_worker_kill()
+            spent += cap_s
+            capped += 1
             k += 1
-            if k % 64 == 0:
-                for job in order[k:k + 64]:
-                    jobs.put(job)
-        else:
-            jobs.put(None)
-            proc.join(timeout=5)
-            if proc.is_alive():
-                proc.kill()
-            break
-        # the worker is stuck on order[k] (over the cap): charge the cap, skip it
-        proc.kill()
-        proc.join()
-        spent += cap_s
-        capped += 1
+            continue
+        if dt > cap_s:   # finished, but beyond the cap: charged the cap only
+            dt = cap_s
+        spent += dt
+        kinds.update(kk)
+        per_w[w] = per_w.get(w, 0) + 1
+        done += 1
         k += 1
     el = max(spent, 1e-9)
     kind = "reference" if kinds == {"reference"} else ("port" if kinds == {"port"} else "reference+port")

@@ -139,7 +139,8 @@ typedef struct {
   int32_t interleave;      /* 1: issue the first ring-full of the largest tcgen05 stream before a small
                               independent stream chain scheduled ahead of it (LoRA's X@A -> T@B), the
                               rest after it: the chain runs while the ring refills */
-  int32_t _reserved[3];
+  int32_t ff_tma;          /* 1: finite-field plans stream their residues through the TMA ring too */
+  int32_t _reserved[2];
 } sgm_plan_hints;
 
 typedef struct {

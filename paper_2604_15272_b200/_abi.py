@@ -43,7 +43,7 @@ class PlanHints(C.Structure):
         ("wd_test", C.c_int32), ("small_plain", C.c_int32), ("big_first", C.c_int32),
         ("item_cost_ns", C.c_int32), ("min_gsplit", C.c_int32),
         ("no_wd", C.c_int32), ("interleave", C.c_int32),
-        ("_reserved", C.c_int32 * 3),
+        ("ff_tma", C.c_int32), ("_reserved", C.c_int32 * 2),
     ]
 
 

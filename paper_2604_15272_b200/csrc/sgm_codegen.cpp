@@ -185,6 +185,9 @@ struct Gen {
   int ilv_big = -1, ilv_pos = -1, ilv_kc = 0, ilv_tmem = 0;
   std::set<int> ilv_chain;
   bool emit_seg1 = false;  // emit_node(ilv_big) emits the first segment (build + MMAs only)
+  // elementwise fusion: fused[n] = n is computed in registers inside its single
+  // elementwise consumer's map (no smem tile write, no barrier)
+  std::vector<char> fused;
   static constexpr int kSlot = 32768;  // largest ring slot; plan_ring may pick 16 KB
   int slotB = 32768;
   static constexpr int kSmemCap = 225 * 1024;  // dynamic smem incl. ring alignment slack
@@ -1153,8 +1156,13 @@ struct Gen {
         const bool batch_ok = x.sl[0] * x.sl[1] <= 8 && b.sl[3] == NN && b.sl[2] == K && (NN * es) % 16 == 0 && !x.inv;
         const i64 sb = stream_bytes(x);
         const bool small = d.hints.small_plain && sb <= 64 * 1024 && sb * 8 <= max_stream;
-        if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 && (ns == SGM_BF16 || ns == SGM_F32) &&
-            !small) {
+        // the finite-field checker can stream its 4-byte residues through the same ring
+        // into the CUDA-core consumer (u64 lazy-reduced accumulators, hints.ff_tma):
+        // measured on the sweep it lost overall (A's FF checks 1.66 -> 3.17 s per step,
+        // L 0.26 -> 0.34; Q 0.76 -> 0.72, R 49 -> 43 ms), so plain loads stay the default
+        const bool ff_ok = ns == SGM_FF && d.hints.ff_tma;
+        if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 &&
+            (ns == SGM_BF16 || ns == SGM_F32 || ff_ok) && !small) {
           if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && (d3 * 2) % 16 == 0 &&
               ntl * 16 <= 512) {
             x.tma = true;
@@ -1174,7 +1182,7 @@ struct Gen {
             int cols = 32;
             while (cols < ntl * x.acc * 16) cols *= 2;
             x.tc_cols = cols;
-          } else if (ns == SGM_F32 && M <= 8 && K % 8 == 0 && NN % 8 == 0 && (d3 * 4) % 16 == 0) {
+          } else if ((ns == SGM_F32 || ns == SGM_FF) && M <= 8 && K % 8 == 0 && NN % 8 == 0 && (d3 * 4) % 16 == 0) {
             x.tma = true;
             ++ntma;
             x.tc = false;
@@ -1187,7 +1195,7 @@ struct Gen {
             // mm_stream_f32 reads a single-batch row-major A in place (DIRECT)
             const bool direct = a0 * a1 == 1 && a.store != ST_VIEW;
             x.at_bytes = direct ? 0 : a0 * a1 * K * M * 4;
-            x.red_bytes = (i64)(NT / 32) * M * 64 * 4;
+            x.red_bytes = (i64)(NT / 32) * M * 64 * ea;
           }
         }
       }
@@ -1866,11 +1874,94 @@ struct Gen {
   // Elementwise map over node n's tile: each thread computes 4 elements into
   // registers before storing any.  In-place ops (output aliasing an operand)
   // otherwise serialise every iteration's loads behind the previous store.
+  static bool elementwise(int k) {
+    return k == SGM_EXP || k == SGM_SILU || k == SGM_SQUARE || k == SGM_SQRT || k == SGM_SCALE || k == SGM_DIV ||
+           k == SGM_MUL || k == SGM_ADD;
+  }
+  bool same_slice(const Node& a, const Node& b) const {
+    for (int k = 0; k < 4; ++k)
+      if (a.sl[k] != b.sl[k]) return false;
+    return true;
+  }
+  i64 tile_end(const Node& x) const { return x.off + prod4(x.sl) * ec; }
+
+  // Elementwise chains fused in registers: node k is evaluated inside the map of
+  // its only consumer y when both are elementwise over the same slice, y comes
+  // right after k in the schedule (same region, no flush or loop boundary in
+  // between), k is not a pending partial, and y's output tile does not overlap
+  // the tiles the fused expression reads (the allocator freed k's operands at k).
+  void plan_fusion() {
+    fused.assign(nodes.size(), 0);
+    if (getenv("SGM_NO_FUSE")) return;
+    std::set<int> flushed;
+    for (auto& e : sched)
+      if (e.type == Ev::FLUSH || e.type == Ev::GFLUSH)
+        for (int f : e.flush) flushed.insert(f);
+    for (int p = 0; p + 1 < (int)sched.size(); ++p) {
+      if (sched[p].type != Ev::NODE || sched[p + 1].type != Ev::NODE) continue;
+      const int k = sched[p].node, y = sched[p + 1].node;
+      const Node& K = nodes[k];
+      const Node& Y = nodes[y];
+      if (!elementwise(K.kind) || !elementwise(Y.kind) || K.cons.size() != 1 || K.cons[0] != y) continue;
+      if (K.store != ST_SMEM || Y.store != ST_SMEM || !same_slice(K, Y) || K.pend || K.gpend || flushed.count(k)) continue;
+      if (K.inv != Y.inv || K.hoist != Y.hoist || K.body != Y.body) continue;
+      // leaves the fused expression reads (k's operands, recursively through fused ones)
+      std::vector<int> leaves, stack = {k};
+      while (!stack.empty()) {
+        const int q = stack.back();
+        stack.pop_back();
+        for (int i = 0; i < nodes[q].nin; ++i) {
+          const int in = nodes[q].in[i];
+          if (fused[in]) stack.push_back(in);
+          else leaves.push_back(in);
+        }
+      }
+      bool ok = true;
+      for (int l : leaves) {
+        const Node& L = nodes[l];
+        if (L.store != ST_SMEM) { ok = false; break; }
+        // y's output over an operand of the fused expression: only element-wise
+        // aliasing (same slice: each element read and written by one thread) is safe
+        if (L.off < tile_end(Y) && Y.off < tile_end(L) && !(same_slice(L, Y) && L.off == Y.off)) { ok = false; break; }
+      }
+      if (ok) fused[k] = 1;
+    }
+  }
+
+  // value of elementwise node n at flat element e (index decomposition i0..i3 of
+  // the slice in scope), with fused operands inlined
+  std::string val_expr(int n) const {
+    const Node& x = nodes[n];
+    auto idx = [&](const Node& a) {
+      i64 sa[4];
+      dense_strides(a.sl, sa);
+      std::ostringstream q;
+      q << "0";
+      const char* iv[4] = {"i0", "i1", "i2", "i3"};
+      for (int k = 0; k < 4; ++k)
+        if (a.sl[k] > 1) q << " + " << iv[k] << " * " << sa[k];
+      return q.str();
+    };
+    auto arg = [&](int k, bool unary) {
+      if (fused[k]) return "(" + val_expr(k) + ")";
+      return tile_ptr(k) + "[" + (unary ? std::string("e") : idx(nodes[k])) + "]";
+    };
+    switch (x.kind) {
+      case SGM_EXP: return "N::ex(" + arg(x.in[0], true) + ")";
+      case SGM_SILU: return "N::silu(" + arg(x.in[0], true) + ")";
+      case SGM_SQUARE: return "N::sq(" + arg(x.in[0], true) + ")";
+      case SGM_SQRT: return "N::sqr(" + arg(x.in[0], true) + ")";
+      case SGM_SCALE: return "N::scale(" + arg(x.in[0], true) + ", (C)" + const_literal(x) + ")";
+      default: {
+        const char* fn = x.kind == SGM_DIV ? "N::div" : x.kind == SGM_MUL ? "N::mul" : "N::add";
+        return std::string(fn) + "(" + arg(x.in[0], false) + ", " + arg(x.in[1], false) + ")";
+      }
+    }
+  }
+
   void emit_map(int n, const std::string& pre, const std::string& expr) {
     const i64 sz = prod4(nodes[n].sl);
     os << "    for (int e0 = tid; e0 < " << sz << "; e0 += 4 * NT) {\n      C v_[4];\n";
-    // compute with the index clamped (no branch around the loads, so the four are
-    // issued back to back); only the stores are guarded
     // guarded (not clamped) reads: a clamped index made out-of-range lanes re-read the
     // last element while its owner wrote it in place (a benign but real smem race,
     // compute-sanitizer racecheck)
@@ -1912,41 +2003,18 @@ struct Gen {
            << tile_ptr(x.in[0]) << ");\n";
         return;  // no barrier needed after a global store
       }
-      case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT: case SGM_SCALE: {
-        const char* fn = x.kind == SGM_EXP ? "N::ex" : x.kind == SGM_SILU ? "N::silu" : x.kind == SGM_SQUARE ? "N::sq" : "N::sqr";
-        std::ostringstream ex;
-        if (x.kind == SGM_SCALE) ex << "N::scale(" << tile_ptr(x.in[0]) << "[e], (C)" << const_literal(x) << ")";
-        else ex << fn << "(" << tile_ptr(x.in[0]) << "[e])";
-        emit_map(n, "", ex.str());
-        break;
-      }
-      case SGM_ACCUM: {
-        emit_map(n, "", "N::add(" + tile_ptr(n) + "[e], " + tile_ptr(x.in[0]) + "[e])");
-        break;
-      }
+      case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT: case SGM_SCALE:
       case SGM_DIV: case SGM_MUL: case SGM_ADD: {
-        const char* fn = x.kind == SGM_DIV ? "N::div" : x.kind == SGM_MUL ? "N::mul" : "N::add";
-        const Node& a = nodes[x.in[0]];
-        const Node& b = nodes[x.in[1]];
-        i64 sa[4], sb[4];
-        dense_strides(a.sl, sa);
-        dense_strides(b.sl, sb);
+        if (fused[n]) return;  // evaluated inside its consumer's map
         std::ostringstream pre;
         pre << "int r = e; const int i3 = r % " << x.sl[3] << "; r /= " << x.sl[3] << "; const int i2 = r % " << x.sl[2]
             << "; r /= " << x.sl[2] << "; const int i1 = r % " << x.sl[1] << "; const int i0 = r / " << x.sl[1]
             << "; (void)i0; (void)i1; (void)i2; (void)i3; ";
-        auto idx = [&](const i64* s, const i64* sl) {
-          std::ostringstream q;
-          q << "0";
-          const char* iv[4] = {"i0", "i1", "i2", "i3"};
-          for (int k = 0; k < 4; ++k)
-            if (sl[k] > 1) q << " + " << iv[k] << " * " << s[k];
-          return q.str();
-        };
-        std::ostringstream ex;
-        ex << fn << "(" << tile_ptr(x.in[0]) << "[" << idx(sa, a.sl) << "], " << tile_ptr(x.in[1]) << "["
-           << idx(sb, b.sl) << "])";
-        emit_map(n, pre.str(), ex.str());
+        emit_map(n, pre.str(), val_expr(n));
+        break;
+      }
+      case SGM_ACCUM: {
+        emit_map(n, "", "N::add(" + tile_ptr(n) + "[e], " + tile_ptr(x.in[0]) + "[e])");
         break;
       }
       case SGM_SUM: {
@@ -2002,9 +2070,9 @@ struct Gen {
              << slotB << ", NT, " << (build ? "true" : "false") << ", " << x.acc << seg << ">(" << tile_ptr(n) << ", " << pa
              << ", sm + " << x.at_off << ", " << tm << ", ring, full, empty, done, sq, sdph);\n";
         } else if (x.tma) {
-          os << "    sgm::mm_stream_f32<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
+          os << "    sgm::mm_stream_f32<N, " << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << x.bw << ", "
-             << ringS << ", " << slotB << ", NT>(" << tile_ptr(n) << ", " << pa << ", (float*)(sm + " << x.at_off << "), (float*)(sm + "
+             << ringS << ", " << slotB << ", NT>(" << tile_ptr(n) << ", " << pa << ", (C*)(sm + " << x.at_off << "), (A*)(sm + "
              << x.red_off << "), ring, full, empty, sq);\n";
         } else if (x.gemv && x.tc) {
           os << "    sgm::mm_gemv_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
@@ -2322,6 +2390,7 @@ struct Gen {
     }
     plan_ring();
     plan_interleave();
+    plan_fusion();
     if (d.hints.trace) {
       trace_off = scratch_per_cta;
       scratch_per_cta += SGM_TRACE_N * 16;
@@ -2368,6 +2437,7 @@ struct Gen {
       TmaSpec t;
       t.slot = x.slot;
       t.elem_bytes = es;
+      t.u32 = ns == SGM_FF;
       t.box0 = x.sbox;
       t.box1 = (int)x.sl[2];
       t.box2 = (int)x.sl[1];
@@ -2384,6 +2454,7 @@ struct Gen {
       TmaSpec t;
       t.slot = b.slot;
       t.elem_bytes = es;
+      t.u32 = ns == SGM_FF;
       t.box0 = x.tc ? 64 : x.bw;
       t.box1 = x.kc;
       t.swizzle128 = x.tc ? 1 : 0;

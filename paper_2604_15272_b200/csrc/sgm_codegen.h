@@ -13,7 +13,8 @@ namespace sgmcg {
 // box1, 1, 1}.
 struct TmaSpec {
   int slot = 0;
-  int elem_bytes = 2;   // 2: bf16, 4: fp32
+  int elem_bytes = 2;   // 2: bf16, 4: fp32 / u32
+  int u32 = 0;          // 4-byte finite-field residues: UINT32 tensor map (bits copied as they are)
   int box0 = 64, box1 = 64, box2 = 1, box3 = 1;
   int swizzle128 = 0;
   int64_t dims[4] = {1, 1, 1, 1};

@@ -1080,11 +1080,21 @@ __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const floa
 // (broadcast within a k-lane) and issues 8*M FMAs.  Partials reduce with
 // shuffles over kq, then across warps through `red` (NW*M*64 floats); each
 // warp's lane 0 releases the slot (empty count = NT/32).
-template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int BW, int S, int SLOT,
-          int NT>
-__device__ __forceinline__ void mm_stream_f32_core(float* __restrict__ out, const float* __restrict__ A,
-                                                float* __restrict__ at, float* __restrict__ red, unsigned char* ring,
-                                                u64* full, u64* empty, u32 q) {
+template <class T> __device__ __forceinline__ T bits_as(u32 v) {
+  if constexpr (same_t<T, float>::v) return __uint_as_float(v);
+  else return (T)v;
+}
+
+template <class N, int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int BW, int S,
+          int SLOT, int NT>
+__device__ __forceinline__ void mm_stream_f32_core(typename N::C* __restrict__ out, const typename N::C* __restrict__ A,
+                                                typename N::C* __restrict__ at, typename N::A* __restrict__ red,
+                                                unsigned char* ring, u64* full, u64* empty, u32 q) {
+  // N = NF32 (fp32 consumer) or NFF (finite-field checker: 4-byte residues stream
+  // through the same ring, u64 lazy-reduced accumulators, mod p at the end)
+  typedef typename N::C C;
+  typedef typename N::A Acc;
+  static_assert(sizeof(C) == 4, "4-byte streamed elements");
   constexpr int NTB = (NN + BW - 1) / BW;
   constexpr int NKC = K / KC;
   constexpr int NW = NT / 32;
@@ -1113,59 +1123,58 @@ __device__ __forceinline__ void mm_stream_f32_core(float* __restrict__ out, cons
   }
   for (int bi = 0; bi < B0 * B1; ++bi) {
     const int b1 = bi % B1, b0 = bi / B1;
-    const float* pa = DIRECT ? A : at + (i64)((SA0 ? b0 : 0) * A1 + (SA1 ? b1 : 0)) * K * M;
+    const C* pa = DIRECT ? A : at + (i64)((SA0 ? b0 : 0) * A1 + (SA1 ? b1 : 0)) * K * M;
 #pragma unroll 1
     for (int t = 0; t < NTB; ++t) {
-      float acc[M][8];
+      Acc acc[M][8];
 #pragma unroll
       for (int m = 0; m < M; ++m)
 #pragma unroll
-        for (int v = 0; v < 8; ++v) acc[m][v] = 0.0f;
+        for (int v = 0; v < 8; ++v) acc[m][v] = N::azero();
 #pragma unroll 1
       for (int kc = 0; kc < NKC; ++kc) {
         const u32 slot = ring_wait<S>(full, q);
-        const float* st = reinterpret_cast<const float*>(ring + slot * SLOT);
+        const C* st = reinterpret_cast<const C*>(ring + slot * SLOT);
         // k-rows kl, kl+KL, ... of the stage, software-pipelined one step ahead so
         // the shared-memory loads of step i+1 overlap the 8*M FMAs of step i (a
         // plain loop left the FMAs waiting on LDS: short-scoreboard stalls in ncu)
         constexpr int NI = (KC + KL - 1) / KL;
-        auto load = [&](int i, float4& w0, float4& w1, float* av) {
+        auto load = [&](int i, uint4& w0, uint4& w1, C* av) {
           const int k = kl + i * KL;
           if (KC % KL != 0 && k >= KC) return;
-          w0 = *reinterpret_cast<const float4*>(st + k * BW + cg * 4);
-          w1 = *reinterpret_cast<const float4*>(st + k * BW + BW / 2 + cg * 4);
+          w0 = *reinterpret_cast<const uint4*>(st + k * BW + cg * 4);
+          w1 = *reinterpret_cast<const uint4*>(st + k * BW + BW / 2 + cg * 4);
           if constexpr (DIRECT) {
 #pragma unroll
             for (int m = 0; m < M; ++m) av[m] = pa[(i64)m * SA2 + kc * KC + k];
             return;
           }
-          const float* ak = pa + (i64)(kc * KC + k) * M;
+          const C* ak = pa + (i64)(kc * KC + k) * M;
           if constexpr (M % 4 == 0) {
 #pragma unroll
-            for (int u = 0; u < M / 4; ++u) *reinterpret_cast<float4*>(&av[u * 4]) = *reinterpret_cast<const float4*>(ak + u * 4);
+            for (int u = 0; u < M / 4; ++u) *reinterpret_cast<uint4*>(&av[u * 4]) = *reinterpret_cast<const uint4*>(ak + u * 4);
           } else {
 #pragma unroll
             for (int m = 0; m < M; ++m) av[m] = ak[m];
           }
         };
-        float4 w0, w1;
-        float av[M];
+        uint4 w0, w1;
+        C av[M];
         load(0, w0, w1, av);
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
-          float4 n0 = w0, n1 = w1;
-          float nav[M];
+          uint4 n0 = w0, n1 = w1;
+          C nav[M];
 #pragma unroll
           for (int m = 0; m < M; ++m) nav[m] = av[m];
           if (i + 1 < NI) load(i + 1, n0, n1, nav);
           if (KC % KL == 0 || kl + i * KL < KC) {
+            const C w[8] = {bits_as<C>(w0.x), bits_as<C>(w0.y), bits_as<C>(w0.z), bits_as<C>(w0.w),
+                            bits_as<C>(w1.x), bits_as<C>(w1.y), bits_as<C>(w1.z), bits_as<C>(w1.w)};
 #pragma unroll
-            for (int m = 0; m < M; ++m) {
-              acc[m][0] = fmaf(av[m], w0.x, acc[m][0]); acc[m][1] = fmaf(av[m], w0.y, acc[m][1]);
-              acc[m][2] = fmaf(av[m], w0.z, acc[m][2]); acc[m][3] = fmaf(av[m], w0.w, acc[m][3]);
-              acc[m][4] = fmaf(av[m], w1.x, acc[m][4]); acc[m][5] = fmaf(av[m], w1.y, acc[m][5]);
-              acc[m][6] = fmaf(av[m], w1.z, acc[m][6]); acc[m][7] = fmaf(av[m], w1.w, acc[m][7]);
-            }
+            for (int m = 0; m < M; ++m)
+#pragma unroll
+              for (int v = 0; v < 8; ++v) N::mac(acc[m][v], av[m], w[v]);
           }
           w0 = n0;
           w1 = n1;
@@ -1180,9 +1189,9 @@ __device__ __forceinline__ void mm_stream_f32_core(float* __restrict__ out, cons
       for (int m = 0; m < M; ++m)
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-          float x = acc[m][v];
+          Acc x = acc[m][v];
 #pragma unroll
-          for (int off = CGN; off < 32; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+          for (int off = CGN; off < 32; off <<= 1) N::amerge(x, shfl_xor(x, off, 0xffffffffu));
           acc[m][v] = x;
         }
       if (kq == 0) {
@@ -1194,23 +1203,23 @@ __device__ __forceinline__ void mm_stream_f32_core(float* __restrict__ out, cons
       csync<NT>();
       for (int e = tid; e < M * BW; e += NT) {
         const int m = e / BW, c = e % BW;
-        float x = 0.0f;
+        Acc x = N::azero();
 #pragma unroll
-        for (int w = 0; w < NW; ++w) x += red[(w * M + m) * BW + c];
+        for (int w = 0; w < NW; ++w) N::amerge(x, red[(w * M + m) * BW + c]);
         const int n = t * BW + c;
-        if (n < NN) out[((i64)bi * M + m) * NN + n] = x;
+        if (n < NN) out[((i64)bi * M + m) * NN + n] = N::fin(x);
       }
       csync<NT>();
     }
   }
 }
 
-template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int BW, int S, int SLOT,
-          int NT>
-__device__ __forceinline__ void mm_stream_f32(float* __restrict__ out, const float* __restrict__ A,
-                                              float* __restrict__ at, float* __restrict__ red, unsigned char* ring,
-                                              u64* full, u64* empty, u32& q) {
-  mm_stream_f32_core<B0, B1, M, K, NN, SA0, SA1, SA2, SA3, KC, BW, S, SLOT, NT>(out, A, at, red, ring, full, empty, q);
+template <class N, int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int BW, int S,
+          int SLOT, int NT>
+__device__ __forceinline__ void mm_stream_f32(typename N::C* __restrict__ out, const typename N::C* __restrict__ A,
+                                              typename N::C* __restrict__ at, typename N::A* __restrict__ red,
+                                              unsigned char* ring, u64* full, u64* empty, u32& q) {
+  mm_stream_f32_core<N, B0, B1, M, K, NN, SA0, SA1, SA2, SA3, KC, BW, S, SLOT, NT>(out, A, at, red, ring, full, empty, q);
   q += (u32)(B0 * B1 * (K / KC) * ((NN + BW - 1) / BW));
 }
 

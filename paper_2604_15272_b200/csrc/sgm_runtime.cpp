@@ -665,7 +665,9 @@ static int encode_tmap(sgm_plan* p, int i, const void* ptr) {
   cuuint32_t box[4] = {(cuuint32_t)t.box0, (cuuint32_t)t.box1, (cuuint32_t)t.box2, (cuuint32_t)t.box3};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = D.cuTensorMapEncodeTiled(&p->tmaps[i],
-                                        t.elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                        t.elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                        : t.u32          ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                         4, const_cast<void*>(ptr), gdim, gstride, box, estr,
                                         CU_TENSOR_MAP_INTERLEAVE_NONE,
                                         t.swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -137,6 +137,7 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.min_gsplit = int(h.get("min_gsplit", 0))
     d.hints.no_wd = int(h.get("no_wd", 0))
     d.hints.interleave = int(h.get("interleave", 0))
+    d.hints.ff_tma = int(h.get("ff_tma", 0))
     return d
 
 

@@ -239,3 +239,29 @@ def test_tile_dump_matches_oracle(S, desk_cases):
                         assert S.rel_err(g, tile) < F64_TOL, (c["id"], coords, idx)
         n += 1
     assert n >= 8
+
+
+@pytest.mark.parametrize("w", ["R", "G", "L"])
+def test_ff_through_the_tma_ring_is_bit_exact(S, w):
+    """hints.ff_tma: finite-field residues streamed through the TMA ring into the
+    CUDA-core consumer (u64 lazy-reduced accumulators) give the program's FF
+    output bit-exactly, repeatedly, at full scale."""
+    import torch
+    from paper_2604_15272_b200 import population as P
+    from paper_2604_15272_b200.ff import ff_fill_inputs, ff_run, ff_trial_seed
+    pop = P.load_population(w)
+    us = P.units(pop)
+    prog = us[0].cand.program
+    ins = ff_fill_inputs(prog, ff_trial_seed(5, 77, 0), 0)
+    exp = ff_run(S.ir.program_candidate(prog), ins, 0)
+    n = 0
+    for u in us[:: max(1, len(us) // 6)]:
+        plan = S.Plan(u.cand, 3, {"ff_tma": 1}, 0)
+        if "mm_stream_f32<N" not in plan.source():
+            continue
+        n += 1
+        for _ in range(2):
+            outs = [torch.empty_like(e) for e in exp]
+            plan.run(ins, outs)
+            assert all(torch.equal(a, b) for a, b in zip(outs, exp)), (w, u.cand.params)
+    assert n >= 1
