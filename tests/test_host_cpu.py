@@ -170,9 +170,14 @@ def test_scaling_prediction_from_costs():
     us = [u for w in ("R", "L") for u in P.units(P.load_population(w))]
     for k, u in enumerate(us):
         u.cost_us = 10.0 + (k * 37) % 11
+        u.dep_us = 0.0                      # no refine share
     pred = P.predict_scaling(us, (2, 4, 8))
     assert 1.9 < pred["2"]["speedup"] <= 2.0 and 7.5 < pred["8"]["speedup"] <= 8.0
     assert P.predict_scaling([u for u in us[:3]] + [P.Unit(0, "R", 0, us[0].cand)], (2,)) == {}
+    for u in us:
+        u.dep_us = 1.0                      # the global top 3 per workload refine 1000 launches each
+    pred = P.predict_scaling(us, (8,))
+    assert pred["8"]["refine_ms"] == 2 * 3 * 1000 * 1.0 / 1e3 and pred["8"]["speedup"] < 8.0
 
 
 def test_population_files_are_reference_searches():
