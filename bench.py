@@ -575,7 +575,11 @@ def main() -> None:
                    "sweep_latency_us": win.latency_us, "candidates": len(wrecs),
                    "failed": sum(1 for r in wrecs if r.error), "ff_mismatch": sum(1 for r in wrecs if r.ff_ok is False),
                    "dep_checked": sum(1 for r in wrecs if r.dep_ok is not None),
-                   "dep_failed": sum(1 for r in wrecs if r.dep_ok is False)}
+                   "dep_failed": sum(1 for r in wrecs if r.dep_ok is False),
+                   # the next tuned kernels (within timing noise of the winner on a rerun):
+                   # their ncu captures back roofline.traffic when a rerun picks one of them
+                   "runners_up": [{"index": r.index, "latency_us": l, "hints": h, "kernel": pl.kernel_name}
+                                  for l, r, h, pl in tuned if pl.kernel_name != plan.kernel_name][:3]}
     if args.best_out:
         with open(args.best_out, "w") as fh:
             json.dump(best, fh, indent=1)

@@ -103,6 +103,9 @@ def main(argv):
             traffic = {}
         kern = traffic.get("kernels", {}) if isinstance(traffic.get("kernels"), dict) else {}
         by_kernel = {b["kernel"]: w for w, b in best.items() if "kernel" in b}
+        for w, b in best.items():
+            for ru in b.get("runners_up", []):
+                by_kernel.setdefault(ru["kernel"], w)
         for rep, rows in res.items():
             for r in rows:
                 w = by_kernel.get(r["kernel"])

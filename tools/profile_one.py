@@ -29,6 +29,10 @@ def main():
         u = next(x for x in us if x.cand.mapping_list() == b["mapping"] and x.cand.params == b["params"]
                  and pop["candidates"][x.pair]["template_id"] == b.get("template", pop["candidates"][x.pair]["template_id"]))
         variant = b.get("hints") or {}
+        if "--runner-up" in sys.argv:  # one of the next tuned kernels of the bench's best-kernel phase
+            ru = b["runners_up"][int(sys.argv[sys.argv.index("--runner-up") + 1])]
+            u = us[ru["index"]]
+            variant = ru.get("hints") or {}
     elif mapping == "best":
         recs = json.load(open(sys.argv[3]))
         rs = [r for r in recs if r["workload"] == w and r["latency_us"] and not r.get("error")]
