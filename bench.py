@@ -267,9 +267,12 @@ def reference_arm(args) -> None:
     if rank != 0:
         return
     workloads = args.workloads
-    per_step = max(4.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    # bounded so the whole --steps K --warmup W run ends within a few minutes: ~100 s of
+    # timed CPU work over the K steps, 1 s per warm-up step (the warm-ups only start
+    # the worker and generate its inputs)
+    per_step = max(3.0, min(20.0, 100.0 / max(1, args.steps)))
     for k in range(args.warmup):
-        cpu_eval_sample(per_step, workloads, seed=10_000 + k)
+        cpu_eval_sample(1.0, workloads, seed=10_000 + k)
     cands, secs, capped = 0, 0.0, 0
     for k in range(args.steps):
         r = cpu_eval_sample(per_step, workloads, seed=k)
