@@ -188,6 +188,10 @@ struct Gen {
   // elementwise fusion: fused[n] = n is computed in registers inside its single
   // elementwise consumer's map (no smem tile write, no barrier)
   std::vector<char> fused;
+  // accumulate-into: acc_first's MMAs land in acc_second's TMEM accumulators (no
+  // read-back of its own), so acc_second's read-back is acc_first + acc_second and
+  // the add node acc_add becomes a copy (LoRA: O = X@W + (X@A)@B)
+  int acc_first = -1, acc_second = -1, acc_add = -1, acc_pre = 0;
   static constexpr int kSlot = 32768;  // largest ring slot; plan_ring may pick 16 KB
   int slotB = 32768;
   static constexpr int kSmemCap = 225 * 1024;  // dynamic smem incl. ring alignment slack
@@ -1903,6 +1907,7 @@ struct Gen {
       const Node& K = nodes[k];
       const Node& Y = nodes[y];
       if (!elementwise(K.kind) || !elementwise(Y.kind) || K.cons.size() != 1 || K.cons[0] != y) continue;
+      if (k == acc_add || y == acc_add) continue;
       if (K.store != ST_SMEM || Y.store != ST_SMEM || !same_slice(K, Y) || K.pend || K.gpend || flushed.count(k)) continue;
       if (K.inv != Y.inv || K.hoist != Y.hoist || K.body != Y.body) continue;
       // leaves the fused expression reads (k's operands, recursively through fused ones)
@@ -1925,6 +1930,37 @@ struct Gen {
         if (L.off < tile_end(Y) && Y.off < tile_end(L) && !(same_slice(L, Y) && L.off == Y.off)) { ok = false; break; }
       }
       if (ok) fused[k] = 1;
+    }
+  }
+
+  void plan_accfuse() {
+    acc_first = acc_second = acc_add = -1;
+    if (getenv("SGM_NO_ACCFUSE") || !prod || ilv_big >= 0) return;
+    std::vector<int> pos(nodes.size(), -1);
+    for (int p = 0; p < (int)sched.size(); ++p)
+      if (sched[p].type == Ev::NODE) pos[sched[p].node] = p;
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      const Node& ad = nodes[n];
+      if (ad.kind != SGM_ADD || ad.inv || ad.body) continue;
+      int a = ad.in[0], b = ad.in[1];
+      if (a == b) continue;
+      const Node& A = nodes[a];
+      const Node& B = nodes[b];
+      auto ok = [&](const Node& m) {
+        return m.kind == SGM_MATMUL && m.tma && m.tc && !m.inv && !m.body && m.cons.size() == 1 &&
+               m.sl[0] * m.sl[1] == 1 && same_slice(m, ad);
+      };
+      if (!ok(A) || !ok(B) || A.acc != B.acc || A.tc_cols != B.tc_cols) continue;
+      if (pos[a] < 0 || pos[b] < 0) continue;
+      int f = pos[a] < pos[b] ? a : b, sec = f == a ? b : a;
+      if (pos[sec] != pos[f] + 1 || pos[n] < pos[sec]) continue;  // adjacent, nothing in between
+      const Node& F = nodes[f];
+      const int nmma = (int)(nodes[F.in[0]].sl[3] / 16);
+      acc_first = f;
+      acc_second = sec;
+      acc_add = n;
+      acc_pre = std::min(F.acc, nmma);
+      return;
     }
   }
 
@@ -2006,6 +2042,10 @@ struct Gen {
       case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT: case SGM_SCALE:
       case SGM_DIV: case SGM_MUL: case SGM_ADD: {
         if (fused[n]) return;  // evaluated inside its consumer's map
+        if (n == acc_add) {  // the sum was formed in TMEM by the accumulate-into pair
+          emit_map(n, "", tile_ptr(acc_second) + "[e]");
+          break;
+        }
         std::ostringstream pre;
         pre << "int r = e; const int i3 = r % " << x.sl[3] << "; r /= " << x.sl[3] << "; const int i2 = r % " << x.sl[2]
             << "; r /= " << x.sl[2] << "; const int i1 = r % " << x.sl[1] << "; const int i0 = r / " << x.sl[1]
@@ -2060,10 +2100,12 @@ struct Gen {
         }
         if (x.tma && x.tc) {
           // interleaved big stream: its first ilv_kc k-chunks were issued before the chain
-          const std::string seg =
+          std::string seg =
               n != ilv_big ? std::string()
                            : emit_seg1 ? ", 0, " + std::to_string(ilv_kc) + ", false"
                                        : ", " + std::to_string(ilv_kc) + ", " + std::to_string(K / x.kc) + ", true";
+          if (n == acc_first) seg = ", 0, " + std::to_string(K / x.kc) + ", false";
+          if (n == acc_second) seg = ", 0, " + std::to_string(K / x.kc) + ", true, " + std::to_string(acc_pre);
           const std::string tm = chain_node ? "tmem_base + " + std::to_string(ilv_tmem) + "u" : std::string("tmem_base");
           os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS << ", "
@@ -2390,6 +2432,7 @@ struct Gen {
     }
     plan_ring();
     plan_interleave();
+    plan_accfuse();
     plan_fusion();
     if (d.hints.trace) {
       trace_off = scratch_per_cta;

@@ -979,15 +979,19 @@ __device__ __forceinline__ void build_xb_g(u16* __restrict__ xb, const u16* __re
 // segments with a small, dependent chain issued in between, see sgm_codegen.cpp
 // interleave); FIN = false issues the segment's MMAs only (accumulators stay in
 // TMEM, no commit to `done`, no read-back).
+// PRE: the first PRE accumulators of each tile already hold an earlier call's
+// product (accumulate-into fusion: LoRA's T@B issued into X@W's accumulators, so
+// one read-back yields X@W + T@B and the add disappears).
 template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int SLOT, int NT,
-          bool BUILD = true, int ACC = 1, int KB = 0, int KE = K / KC, bool FIN = true>
+          bool BUILD = true, int ACC = 1, int KB = 0, int KE = K / KC, bool FIN = true, int PRE = 0>
 __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const float* __restrict__ A,
                                                unsigned char* __restrict__ xbuf, u32 tmem, unsigned char* ring,
                                                u64* full, u64* empty, u64* done, u32 q, u32 dph) {
   constexpr int NTL = (NN + 127) / 128;
   constexpr int NKC = KE - KB;
-  static_assert(KB == 0 && KE == K / KC && FIN || (B0 * B1 == 1 && !BUILD && 0 <= KB && KB < KE && KE <= K / KC),
-                "segmented stream: one batch, prebuilt A^T");
+  static_assert((KB == 0 && KE == K / KC && FIN && PRE == 0) ||
+                    (B0 * B1 == 1 && (!BUILD || (KB == 0 && KE == K / KC)) && 0 <= KB && KB < KE && KE <= K / KC),
+                "segmented / accumulate-into stream: one batch");
   constexpr bool SPLIT = M <= 8;
   constexpr u32 IDESC = UMMA_IDESC_BF16_M128_N16;
   constexpr int NMMA = K / 16;                      // MMAs per tile
@@ -1025,7 +1029,7 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
             const u64 ad = umma_desc_sw128(st + ks * 2048, LBO, 1024);
             const u64 bd = umma_desc(xs + ((kc * KC + ks * 16) >> 3) * 256, 256, 128);
             const int g = kc * (KC / 16) + ks;  // MMA index along K
-            umma_bf16(tmem + (t * ACC + g % AC) * 16, ad, bd, IDESC, g >= AC);
+            umma_bf16(tmem + (t * ACC + g % AC) * 16, ad, bd, IDESC, g >= AC || g < PRE);
           }
           umma_commit(&empty[slot]);
         }
@@ -1061,11 +1065,11 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
 // Out of line (one copy per shape): a kernel's later calls of the same shape run
 // from a warm instruction cache; the ring/phase counters advance deterministically.
 template <int B0, int B1, int M, int K, int NN, i64 SA0, i64 SA1, i64 SA2, i64 SA3, int KC, int S, int SLOT, int NT,
-          bool BUILD = true, int ACC = 1, int KB = 0, int KE = K / KC, bool FIN = true>
+          bool BUILD = true, int ACC = 1, int KB = 0, int KE = K / KC, bool FIN = true, int PRE = 0>
 __device__ __forceinline__ void mm_stream_tc(float* __restrict__ out, const float* __restrict__ A,
                                              unsigned char* __restrict__ xbuf, u32 tmem, unsigned char* ring, u64* full,
                                              u64* empty, u64* done, u32& q, u32& dph) {
-  mm_stream_tc_core<B0, B1, M, K, NN, SA0, SA1, SA2, SA3, KC, S, SLOT, NT, BUILD, ACC, KB, KE, FIN>(
+  mm_stream_tc_core<B0, B1, M, K, NN, SA0, SA1, SA2, SA3, KC, S, SLOT, NT, BUILD, ACC, KB, KE, FIN, PRE>(
       out, A, xbuf, tmem, ring, full, empty, done, q, dph);
   q += (u32)(B0 * B1 * (KE - KB) * ((NN + 127) / 128));
   if constexpr (FIN) dph ^= (u32)((B0 * B1) & 1);
