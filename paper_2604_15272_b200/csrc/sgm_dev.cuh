@@ -185,7 +185,14 @@ struct NFF {
   __device__ static __forceinline__ void amerge(A& a, A b) { a += b; }
   __device__ static __forceinline__ void mac(A& a, C x, C y) { a += ff_mul_lazy(x, y); }  // < 2^32 per term
   __device__ static __forceinline__ C fin(A a) { return modp64(a); }
+  // streamed contractions: raw 62-bit products accumulated with one IMAD.WIDE each,
+  // folded below 2^34 every FOLD products ((2^31-1)^2 * 3 + 2^34 < 2^64)
+  static constexpr int FOLD = 3;
+  __device__ static __forceinline__ void mac_raw(A& a, C x, C y) { a += (u64)x * y; }
+  __device__ static __forceinline__ void fold(A& a) { a = (a & P) + (a >> 31); }
 };
+template <class N> struct has_fold { static constexpr bool v = false; };
+template <> struct has_fold<NFF> { static constexpr bool v = true; };
 
 // Storage -> compute conversion usable on either a smem tile (C) or a global view (S).
 template <class X, class Y> struct same_t { static constexpr bool v = false; };
@@ -415,7 +422,16 @@ __device__ __forceinline__ void mm_generic(typename N::C* __restrict__ out, cons
     const TA* pa = A + b0 * SA0 + b1 * SA1 + (i64)m * SA2;
     const TB* pb = B + b0 * SB0 + b1 * SB1 + (i64)n * SB3;
     Acc acc = N::azero();
-    for (int k = tid % TPO; k < K; k += TPO) N::mac(acc, cvs<N>(pa[(i64)k * SA3]), cvs<N>(pb[(i64)k * SB2]));
+    int k = tid % TPO;
+    if constexpr (has_fold<N>::v) {  // finite field: 3 raw products per fold
+      for (; k + 2 * TPO < K; k += 3 * TPO) {
+        N::mac_raw(acc, cvs<N>(pa[(i64)k * SA3]), cvs<N>(pb[(i64)k * SB2]));
+        N::mac_raw(acc, cvs<N>(pa[(i64)(k + TPO) * SA3]), cvs<N>(pb[(i64)(k + TPO) * SB2]));
+        N::mac_raw(acc, cvs<N>(pa[(i64)(k + 2 * TPO) * SA3]), cvs<N>(pb[(i64)(k + 2 * TPO) * SB2]));
+        N::fold(acc);
+      }
+    }
+    for (; k < K; k += TPO) N::mac(acc, cvs<N>(pa[(i64)k * SA3]), cvs<N>(pb[(i64)k * SB2]));
 #pragma unroll
     for (int off = TPO / 2; off > 0; off >>= 1) N::amerge(acc, shfl_xor(acc, off, gmask));
     if ((tid % TPO) == 0) out[o] = N::fin(acc);
@@ -516,7 +532,18 @@ __device__ __forceinline__ void mm_gemv(typename N::C* __restrict__ out, const t
 #pragma unroll
           for (int m = 0; m < M; ++m) {
 #pragma unroll
-            for (int v = 0; v < VN; ++v) N::mac(acc[m][v], av[m], bc[v]);
+            for (int v = 0; v < VN; ++v) {
+              if constexpr (has_fold<N>::v) N::mac_raw(acc[m][v], av[m], bc[v]);
+              else N::mac(acc[m][v], av[m], bc[v]);
+            }
+          }
+        }
+        if constexpr (has_fold<N>::v) {
+          if (u % N::FOLD == N::FOLD - 1 || u == UNR - 1) {
+#pragma unroll
+            for (int m = 0; m < M; ++m)
+#pragma unroll
+              for (int v = 0; v < VN; ++v) N::fold(acc[m][v]);
           }
         }
       }

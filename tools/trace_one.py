@@ -61,14 +61,14 @@ def pick(w, mapping, arg):
 
 def main():
     w, mapping, arg = sys.argv[1:4]
-    hints = json.loads(sys.argv[4]) if len(sys.argv) > 4 else {}
+    hints = json.loads(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].startswith("{") else {}
     hints["trace"] = 1
     pop, u, variant = pick(w, mapping, arg)
     for k, v in (variant or {}).items():
         hints.setdefault(k, v)
     torch.cuda.set_device(0)
     _abi.bind_device(0)
-    ns = P.numsys_of(pop["dtype"])
+    ns = _abi.FF if "--ff" in sys.argv else P.numsys_of(pop["dtype"])
     plan = Plan(u.cand, ns, hints, 0)
     ws = workspace(u.cand.program, ns, 0)
     for i in range(4):
