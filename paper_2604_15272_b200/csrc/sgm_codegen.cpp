@@ -192,6 +192,10 @@ struct Gen {
   // read-back of its own), so acc_second's read-back is acc_first + acc_second and
   // the add node acc_add becomes a copy (LoRA: O = X@W + (X@A)@B)
   int acc_first = -1, acc_second = -1, acc_add = -1, acc_pre = 0;
+  // finite field: a broadcast divisor tile consumed only by one div is inverted in
+  // place once (Fermat inverse, ~60 modular products) and the div becomes a mul,
+  // instead of one inverse per numerator element (QK-norm's [128, L] / [1, L])
+  std::vector<char> inv_first;
   static constexpr int kSlot = 32768;  // largest ring slot; plan_ring may pick 16 KB
   int slotB = 32768;
   static constexpr int kSmemCap = 225 * 1024;  // dynamic smem incl. ring alignment slack
@@ -1164,7 +1168,8 @@ struct Gen {
         // into the CUDA-core consumer (u64 lazy-reduced accumulators, hints.ff_tma):
         // measured on the sweep it lost overall (A's FF checks 1.66 -> 3.17 s per step,
         // L 0.26 -> 0.34; Q 0.76 -> 0.72, R 49 -> 43 ms), so plain loads stay the default
-        const bool ff_ok = ns == SGM_FF && d.hints.ff_tma;
+        static const bool ff_tma_env = getenv("SGM_FF_TMA") != nullptr;  // A/B experiments
+        const bool ff_ok = ns == SGM_FF && (d.hints.ff_tma || ff_tma_env);
         if (!d.hints.no_tma && !no_tma_forced && batch_ok && ntma < 4 &&
             (ns == SGM_BF16 || ns == SGM_F32 || ff_ok) && !small) {
           if (ns == SGM_BF16 && d.hints.use_tcgen05 >= 0 && M <= 16 && K % 16 == 0 && (d3 * 2) % 16 == 0 &&
@@ -1964,6 +1969,20 @@ struct Gen {
     }
   }
 
+  void plan_inv() {
+    inv_first.assign(nodes.size(), 0);
+    if (ns != SGM_FF || getenv("SGM_NO_INVFIRST")) return;
+    for (auto& d : nodes) {
+      if (d.kind != SGM_DIV) continue;
+      const int bi = d.in[1];
+      const Node& b = nodes[bi];
+      if (d.in[0] == bi || b.store != ST_SMEM || b.cons.size() != 1 || fused[bi] || b.pend || b.gpend) continue;
+      if (prod4(b.sl) >= prod4(d.sl) || b.inv != d.inv || b.hoist != d.hoist || b.body != d.body) continue;
+      if (b.kind == SGM_INPUT && b.staged) continue;
+      inv_first[bi] = 1;
+    }
+  }
+
   // value of elementwise node n at flat element e (index decomposition i0..i3 of
   // the slice in scope), with fused operands inlined
   std::string val_expr(int n) const {
@@ -1989,7 +2008,8 @@ struct Gen {
       case SGM_SQRT: return "N::sqr(" + arg(x.in[0], true) + ")";
       case SGM_SCALE: return "N::scale(" + arg(x.in[0], true) + ", (C)" + const_literal(x) + ")";
       default: {
-        const char* fn = x.kind == SGM_DIV ? "N::div" : x.kind == SGM_MUL ? "N::mul" : "N::add";
+        const char* fn = x.kind == SGM_DIV ? (inv_first[x.in[1]] ? "N::mul" : "N::div")
+                         : x.kind == SGM_MUL ? "N::mul" : "N::add";
         return std::string(fn) + "(" + arg(x.in[0], false) + ", " + arg(x.in[1], false) + ")";
       }
     }
@@ -2041,6 +2061,11 @@ struct Gen {
       }
       case SGM_EXP: case SGM_SILU: case SGM_SQUARE: case SGM_SQRT: case SGM_SCALE:
       case SGM_DIV: case SGM_MUL: case SGM_ADD: {
+        if (x.kind == SGM_DIV && inv_first[x.in[1]]) {  // invert the divisor tile once, in place
+          const i64 sz = prod4(nodes[x.in[1]].sl);
+          os << "    for (int e = tid; e < " << sz << "; e += NT) " << tile_ptr(x.in[1]) << "[e] = N::inv("
+             << tile_ptr(x.in[1]) << "[e]);\n    sgm::csync<NT>();\n";
+        }
         if (fused[n]) return;  // evaluated inside its consumer's map
         if (n == acc_add) {  // the sum was formed in TMEM by the accumulate-into pair
           emit_map(n, "", tile_ptr(acc_second) + "[e]");
@@ -2434,6 +2459,7 @@ struct Gen {
     plan_interleave();
     plan_accfuse();
     plan_fusion();
+    plan_inv();
     if (d.hints.trace) {
       trace_off = scratch_per_cta;
       scratch_per_cta += SGM_TRACE_N * 16;

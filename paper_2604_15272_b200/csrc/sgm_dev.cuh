@@ -187,6 +187,7 @@ struct NFF {
   __device__ static __forceinline__ C fin(A a) { return modp64(a); }
   // streamed contractions: raw 62-bit products accumulated with one IMAD.WIDE each,
   // folded below 2^34 every FOLD products ((2^31-1)^2 * 3 + 2^34 < 2^64)
+  __device__ static __forceinline__ C inv(C a) { return ff_inv(a); }
   static constexpr int FOLD = 3;
   __device__ static __forceinline__ void mac_raw(A& a, C x, C y) { a += (u64)x * y; }
   __device__ static __forceinline__ void fold(A& a) { a = (a & P) + (a >> 31); }
@@ -1205,7 +1206,18 @@ __device__ __forceinline__ void mm_stream_f32_core(typename N::C* __restrict__ o
 #pragma unroll
             for (int m = 0; m < M; ++m)
 #pragma unroll
-              for (int v = 0; v < 8; ++v) N::mac(acc[m][v], av[m], w[v]);
+              for (int v = 0; v < 8; ++v) {
+                if constexpr (has_fold<N>::v) N::mac_raw(acc[m][v], av[m], w[v]);
+                else N::mac(acc[m][v], av[m], w[v]);
+              }
+          }
+          if constexpr (has_fold<N>::v) {
+            if (i % N::FOLD == N::FOLD - 1 || i == NI - 1) {
+#pragma unroll
+              for (int m = 0; m < M; ++m)
+#pragma unroll
+                for (int v = 0; v < 8; ++v) N::fold(acc[m][v]);
+            }
           }
           w0 = n0;
           w1 = n1;
