@@ -140,7 +140,8 @@ typedef struct {
                               independent stream chain scheduled ahead of it (LoRA's X@A -> T@B), the
                               rest after it: the chain runs while the ring refills */
   int32_t ff_tma;          /* 1: finite-field plans stream their residues through the TMA ring too */
-  int32_t _reserved[2];
+  int32_t no_xcache;       /* 1: no x-cache (nodes independent of the grid coordinate recomputed per item) */
+  int32_t _reserved[1];
 } sgm_plan_hints;
 
 typedef struct {

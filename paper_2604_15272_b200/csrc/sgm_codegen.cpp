@@ -107,6 +107,8 @@ struct Node {
   bool staged = false;     // loader tile fetched by the producer (TMA) into a staging buffer
   int stage_id = -1, stage_off = 0, sbox = 0;
   bool inv = false;        // item-invariant: computed once per CTA, before the item loop
+  bool xc = false;         // x-cached: independent of the grid coordinate; recomputed only when the
+                           // item's other coordinates change (items run gx-fastest, contiguous per CTA)
   bool xb_shared = false;  // tcgen05 A^T buffer shared per A node (batch 1)
   bool xb_build = true;    // this consumer (re)builds the shared A^T buffer
 };
@@ -196,6 +198,11 @@ struct Gen {
   // place once (Fermat inverse, ~60 modular products) and the div becomes a mul,
   // instead of one inverse per numerator element (QK-norm's [128, L] / [1, L])
   std::vector<char> inv_first;
+  // x-cache: some nodes (>= one matmul) do not depend on the grid coordinate gx
+  // (e.g. attention scores when only the head dim of V/O is split, LoRA's X@A when
+  // only output columns are): each CTA runs a contiguous range of items gx-fastest
+  // and recomputes those nodes only when the item's other coordinates change
+  bool xcache = false, xcache_loop = false;
   static constexpr int kSlot = 32768;  // largest ring slot; plan_ring may pick 16 KB
   int slotB = 32768;
   static constexpr int kSmemCap = 225 * 1024;  // dynamic smem incl. ring alignment slack
@@ -625,6 +632,7 @@ struct Gen {
     // shared-memory feasibility of this split (tiles + A^T buffers + a minimal ring)
     invariants();
     matmul_choices();
+    plan_xcache();
     const int peak = allocate();
     const int cap = prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024) - (int)stage_total) : budget;
     // soft penalty (10 us per KB over) so the search can walk out of infeasible splits
@@ -660,6 +668,8 @@ struct Gen {
         item_dep = item_dep || (c >= 0 && cls[c].parts > 1 && !cls[c].cluster);
       }
       double execs = item_dep ? (double)items * CL : (double)active;
+      // x-cached loaders are re-read only when a CTA's item moves to other coordinates
+      if (xcache && x.xc) execs = std::min(execs, (double)items / (double)grid[0] + (double)active);
       total += per * reps * execs;
     }
     double redundant = std::max(0.0, total - unique);
@@ -1340,9 +1350,10 @@ struct Gen {
       const Node& x = nodes[n];
       const bool ew = x.kind == SGM_EXP || x.kind == SGM_SILU || x.kind == SGM_SQUARE || x.kind == SGM_SQRT ||
                       x.kind == SGM_SCALE || x.kind == SGM_DIV || x.kind == SGM_MUL || x.kind == SGM_ADD;
-      if (!ew || x.store != ST_SMEM || x.inv || d.hints.no_hoist) continue;
+      if (!ew || x.store != ST_SMEM || x.inv || x.xc || d.hints.no_hoist) continue;
       const Node& a = nodes[x.in[0]];
-      bool same = a.store == ST_SMEM && a.kind != SGM_ACCUM && a.kind != SGM_INPUT && !a.inv && last[x.in[0]] == p;
+      bool same = a.store == ST_SMEM && a.kind != SGM_ACCUM && a.kind != SGM_INPUT && !a.inv && !a.xc &&
+                  last[x.in[0]] == p;
       for (int k = 0; k < 4 && same; ++k) same = a.sl[k] == x.sl[k];
       if (x.nin == 2 && x.in[1] != x.in[0] && rep[x.in[1]] == rep[x.in[0]]) same = false;
       if (same) rep[n] = rep[x.in[0]];
@@ -1356,7 +1367,7 @@ struct Gen {
       int en = std::max(last[n], pos_of[n]);
       if (loop_begin_pos >= 0 && st < loop_begin_pos && en > loop_begin_pos) en = std::max(en, loop_end_pos);
       if (x.kind == SGM_ACCUM) en = std::max(en, loop_end_pos);
-      if (x.inv) { st = 0; en = S; }  // lives across all items
+      if (x.inv || x.xc) { st = 0; en = S; }  // lives across items
       auto it = groups.find(rep[n]);
       if (it == groups.end()) {
         Interval I;
@@ -1477,6 +1488,66 @@ struct Gen {
     return (int)peak;
   }
 
+  void plan_xcache() {
+    for (auto& x : nodes) x.xc = false;
+    xcache = xcache_loop = false;
+    if (getenv("SGM_NO_XCACHE") || d.hints.no_xcache || d.hints.interleave || CL != 1 || ngrid != 1 ||
+        grid[0] <= 1)
+      return;
+    std::vector<char> dep(nodes.size(), 0);
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      const Node& x = nodes[n];
+      if (x.kind == SGM_INPUT) {
+        for (int k = 0; k < 4; ++k) dep[n] = dep[n] || (x.gmask[k] & 1u);
+      } else if (x.kind == SGM_OUTPUT) {
+        dep[n] = 1;
+      } else {
+        for (int k = 0; k < x.nin; ++k) dep[n] = dep[n] || dep[x.in[k]];
+      }
+    }
+    bool loop_inv = true, has_body = false;
+    for (int n = 0; n < (int)nodes.size(); ++n)
+      if (nodes[n].body && !nodes[n].hoist) { has_body = true; loop_inv = loop_inv && !dep[n]; }
+    std::set<int> flushed;
+    for (auto& e : sched)
+      if (e.type == Ev::FLUSH || e.type == Ev::GFLUSH)
+        for (int f : e.flush) flushed.insert(f);
+    int mm = 0;
+    for (int n = 0; n < (int)nodes.size(); ++n) {
+      Node& x = nodes[n];
+      if (dep[n] || x.inv || x.kind == SGM_OUTPUT || x.staged || x.pend || x.gpend || flushed.count(n)) continue;
+      if (x.body && !x.hoist && !loop_inv) continue;
+      if (x.store == ST_GLOBAL) continue;
+      x.xc = true;
+      if (x.kind == SGM_MATMUL) ++mm;
+    }
+    if (!mm) {
+      for (auto& x : nodes) x.xc = false;
+      return;
+    }
+    xcache = true;
+    xcache_loop = has_body && loop_inv;
+  }
+
+  // item loop header: the default round-robin order, or (x-cache) a contiguous
+  // range of items per CTA run gx-fastest, with xc_miss = the other coordinates changed
+  void emit_item_loop(const char* ind, const char* counter) {
+    const i64 T = LB * FP * GP;
+    if (!xcache) {
+      os << ind << "for (long long item = cid; item < " << T << "LL; item += ncl, ++" << counter << ") {\n";
+      emit_item_vars(ind);
+      return;
+    }
+    os << ind << "long long xc_f = -1, xc_g = -1;\n";
+    os << ind << "const long long xc_lo = cid * " << T << "LL / ncl, xc_hi = (cid + 1) * " << T << "LL / ncl;\n";
+    os << ind << "for (long long xc_t = xc_lo; xc_t < xc_hi; ++xc_t, ++" << counter << ") {\n";
+    os << ind << "const long long xc_gx = xc_t % " << grid[0] << "LL, xc_r = xc_t / " << grid[0] << "LL;\n";
+    os << ind << "const long long item = (xc_r % " << GP << "LL) + " << GP << "LL * ((xc_r / " << GP << "LL) + " << FP
+       << "LL * xc_gx);\n";
+    emit_item_vars(ind);
+    os << ind << "const bool xc_miss = fpart != xc_f || gpart != xc_g; xc_f = fpart; xc_g = gpart;\n";
+  }
+
   bool fit() {
     // grow splits on the largest tile while over budget, then spill to global
     for (int iter = 0; iter < 64; ++iter) {
@@ -1484,6 +1555,7 @@ struct Gen {
       schedule();
       invariants();
       matmul_choices();
+      plan_xcache();
       smem_peak = allocate();
       const int tile_budget = prod ? std::min(budget, kSmemCap - (3 * 16384 + 1024) - (int)stage_total) : budget;
       if (smem_peak <= tile_budget) return true;
@@ -1707,8 +1779,7 @@ struct Gen {
     if (d.hints.wd_test) os << "      return;  // wd_test: nothing is streamed, every ring wait must time out\n";
     if (getenv("SGM_LATE_STREAM")) os << "      sgm::mbar_wait(go, 0);\n";
     os << "      unsigned pit = 0;\n";
-    os << "      for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl, ++pit) {\n";
-    emit_item_vars("      ");
+    emit_item_loop("      ", "pit");
     os << "      SGM_TRP(3);\n";
     for (auto& x : nodes) {
       if (!x.staged) continue;
@@ -1726,15 +1797,21 @@ struct Gen {
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
       if (e.type == Ev::LOOP_BEGIN) {
+        if (xcache_loop) os << "      if (xc_miss) {\n";
         os << "      for (int j = jp * " << nloop / LP << "; j < (jp + 1) * " << nloop / LP << "; ++j) {\n";
         in_loop = true;
       } else if (e.type == Ev::LOOP_END) {
         os << "      }\n";
+        if (xcache_loop) os << "      }\n";
         in_loop = false;
       } else if (e.type == Ev::NODE) {
         if (p == ilv_pos) emit_producer_node(ilv_big, in_loop, 0, ilv_kc);
-        if (nodes[e.node].kind == SGM_MATMUL && nodes[e.node].tma)
+        if (nodes[e.node].kind == SGM_MATMUL && nodes[e.node].tma) {
+          const bool wrap = nodes[e.node].xc && !(in_loop && xcache_loop);
+          if (wrap) os << "      if (xc_miss) {\n";
           emit_producer_node(e.node, in_loop, e.node == ilv_big ? ilv_kc : 0);
+          if (wrap) os << "      }\n";
+        }
       }
     }
     os << "      }\n      SGM_TRP(6);\n    }\n    return;\n";
@@ -1955,7 +2032,7 @@ struct Gen {
         return m.kind == SGM_MATMUL && m.tma && m.tc && !m.inv && !m.body && m.cons.size() == 1 &&
                m.sl[0] * m.sl[1] == 1 && same_slice(m, ad);
       };
-      if (!ok(A) || !ok(B) || A.acc != B.acc || A.tc_cols != B.tc_cols) continue;
+      if (!ok(A) || !ok(B) || A.acc != B.acc || A.tc_cols != B.tc_cols || A.xc || B.xc) continue;
       if (pos[a] < 0 || pos[b] < 0) continue;
       int f = pos[a] < pos[b] ? a : b, sec = f == a ? b : a;
       if (pos[sec] != pos[f] + 1 || pos[n] < pos[sec]) continue;  // adjacent, nothing in between
@@ -2320,13 +2397,13 @@ struct Gen {
     bool gs_open = false;
     if (GP > 1) os << "  __shared__ unsigned sgm_last;\n";
     os << "  unsigned cit = 0; (void)cit;\n";
-    os << "  for (long long item = cid; item < " << LB * FP * GP << "LL; item += ncl, ++cit) {\n";
-    emit_item_vars("  ");
+    emit_item_loop("  ", "cit");
     os << "  SGM_TR(2);\n";
     bool in_loop = false;
     for (int p = 0; p < (int)sched.size(); ++p) {
       const Ev& e = sched[p];
       if (e.type == Ev::LOOP_BEGIN) {
+        if (xcache_loop) os << "  if (xc_miss) {  // the whole loop is independent of gx\n";
         for (int n = 0; n < (int)nodes.size(); ++n)
           if (nodes[n].kind == SGM_ACCUM)
             os << "  for (int e = tid; e < " << prod4(nodes[n].sl) << "; e += NT) " << tile_ptr(n) << "[e] = N::zero();\n";
@@ -2339,6 +2416,7 @@ struct Gen {
         in_loop = true;
       } else if (e.type == Ev::LOOP_END) {
         os << "  }\n";
+        if (xcache_loop) os << "  }\n";
         in_loop = false;
       } else if (e.type == Ev::FLUSH) {
         os << "  SGM_TR(" << 2000 + p << ");\n";
@@ -2355,6 +2433,8 @@ struct Gen {
           emit_seg1 = false;
         }
         if (nodes[e.node].kind == SGM_MATMUL || nodes[e.node].kind == SGM_SUM) os << "  SGM_TR(" << 1000 + e.node << ");\n";
+        const bool xwrap = nodes[e.node].xc && !(in_loop && xcache_loop);
+        if (xwrap) os << "  if (xc_miss) {  // independent of gx: kept from the previous item\n";
         if (d.hints.trace) {  // thread 0's own share done (before the node's closing barrier)
           std::ostringstream keep;
           keep << os.str();
@@ -2369,6 +2449,7 @@ struct Gen {
         } else {
           emit_node(e.node, in_loop);
         }
+        if (xwrap) os << "  }\n";
       }
     }
     if (gs_open) os << "  }  // last work item of the reduction group\n";

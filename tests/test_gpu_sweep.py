@@ -81,3 +81,38 @@ def test_split_plans_agree_exactly_in_the_field(S, w, mapping, params, hints):
         plan.run(ins, outs)
         for g, e in zip(outs, exp):
             assert torch.equal(g, e), (w, hints, plan.info["summary"])
+
+
+@pytest.mark.parametrize("w,mapping", [("Q", "O.3.x,V.3.x"), ("A", "Kt.2.i,O.3.x,Q.3.i,V.3.x")])
+@pytest.mark.parametrize("x", [2, 16, 128])
+def test_x_cache_is_exact(S, w, mapping, x):
+    """x-cache: nodes independent of the grid coordinate (the attention scores when
+    only V/O's head dim is split) are kept across a CTA's consecutive items and
+    recomputed only when the other coordinates change.  FF bit-exact against the
+    program (twice: cache state across launches), deployment dtype against the
+    fp64 oracle."""
+    import torch
+    from oracle import block_np
+    from paper_2604_15272_b200 import population as P
+    from paper_2604_15272_b200.ff import ff_fill_inputs, ff_run, ff_trial_seed
+    pop = P.load_population(w)
+    u = next(v for v in P.units(pop) if v.cand.mapping_list() == sorted(mapping.split(","))
+             and v.cand.params == {"x": x, "i": 1})
+    prog = u.cand.program
+    ins = ff_fill_inputs(prog, ff_trial_seed(9, x, 0), 0)
+    exp = ff_run(S.ir.program_candidate(prog), ins, 0)
+    plan = S.Plan(u.cand, 3, None, 0)
+    assert "xc_miss" in plan.source()
+    for _ in range(2):
+        outs = [torch.empty_like(e) for e in exp]
+        plan.run(ins, outs)
+        assert all(torch.equal(a, b) for a, b in zip(outs, exp)), (w, x)
+    dt = pop["dtype"]
+    assert "xc_miss" in S.Plan(u.cand, 2, None, None).source()
+    rng = np.random.default_rng(31)
+    progd = pop["program"]
+    ins_d = {t["name"]: torch.from_numpy(rng.standard_normal(tuple(t["dims"]))).bfloat16().double().numpy()
+             for t in progd["tensors"] if t["role"] == "input"}
+    ref = block_np.run_program(progd, ins_d)
+    got = S.run_concrete(u.cand, ins_d, dtype=dt)
+    assert S.rel_err(got["O"], ref["O"]) < 1e-2, (w, x)
