@@ -141,7 +141,8 @@ typedef struct {
                               rest after it: the chain runs while the ring refills */
   int32_t ff_tma;          /* 1: finite-field plans stream their residues through the TMA ring too */
   int32_t no_xcache;       /* 1: no x-cache (nodes independent of the grid coordinate recomputed per item) */
-  int32_t _reserved[1];
+  int32_t no_prefetch;     /* 1: loop-body tiles are not prefetched into registers one iteration ahead */
+  int32_t _reserved[3];
 } sgm_plan_hints;
 
 typedef struct {

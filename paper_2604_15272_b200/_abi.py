@@ -43,8 +43,8 @@ class PlanHints(C.Structure):
         ("wd_test", C.c_int32), ("small_plain", C.c_int32), ("big_first", C.c_int32),
         ("item_cost_ns", C.c_int32), ("min_gsplit", C.c_int32),
         ("no_wd", C.c_int32), ("interleave", C.c_int32),
-        ("ff_tma", C.c_int32), ("no_xcache", C.c_int32),
-        ("_reserved", C.c_int32 * 1),
+        ("ff_tma", C.c_int32), ("no_xcache", C.c_int32), ("no_prefetch", C.c_int32),
+        ("_reserved", C.c_int32 * 3),
     ]
 
 

@@ -705,7 +705,7 @@ struct Gen {
 
   // Beam search from no split (width 4): each step doubles one class (in an
   // allowed mode) or the loop; `policy` restricts the mode of reduced classes and
-  // the loop (0: either, 1: cluster only, 2: gsplit only).  A plain greedy
+  // the loop (0: either, 1: cluster only, 2: gsplit only, 3: not split).  A plain greedy
   // descent gets trapped by early shared-memory-driven choices (e.g. splitting a
   // GEMV's rows, which multiplies the weight stream).
   double greedy(int policy, PlanState& out) {
@@ -730,8 +730,10 @@ struct Gen {
     seen.insert(key(root));
     double best = root_cost;
     PlanState best_st = root;
-    const std::vector<int> rmodes =
-        policy == 1 ? std::vector<int>{1} : policy == 2 ? std::vector<int>{2} : std::vector<int>{1, 2};
+    const std::vector<int> rmodes = policy == 1   ? std::vector<int>{1}
+                                    : policy == 2 ? std::vector<int>{2}
+                                    : policy == 3 ? std::vector<int>{}
+                                                  : std::vector<int>{1, 2};
     for (int iter = 0; iter < 40; ++iter) {
       std::vector<std::pair<double, PlanState>> next;
       auto consider = [&](const PlanState& st) {
@@ -764,7 +766,7 @@ struct Gen {
             consider(st);
           }
         }
-        if (loop_split_ok && nloop % (cur.lp * 2) == 0) {
+        if (loop_split_ok && policy != 3 && nloop % (cur.lp * 2) == 0) {
           std::vector<int> modes = cur.lp > 1 ? std::vector<int>{cur.lmode} : rmodes;
           for (int m : modes) {
             PlanState st = cur;
@@ -795,12 +797,16 @@ struct Gen {
     PlanState best_st;
     double best = 1e30;
     pool.clear();
-    // gsplit-only first: cluster plans must win by 10% (their flush and GPC-placement
-    // costs are the least well modelled, measured 3-7 us per item)
-    for (int policy : {2, 1, 0}) {
+    // free splits only, then gsplit-only: cluster plans must win by 10% (their flush and
+    // GPC-placement costs are the least well modelled, measured 3-7 us per item).  The
+    // free-only descent matters when splitting the reductions first pulls the other beams
+    // away from a many-item plan that only the x-cache makes cheap (Q's head-dim splits)
+    static const bool no_free = getenv("SGM_NO_FREE_POLICY") != nullptr;  // A/B experiments
+    for (int policy : {3, 2, 1, 0}) {
+      if (policy == 3 && no_free) continue;
       PlanState st;
       double c = greedy(policy, st);
-      if (c < best * (policy == 2 ? 1.0 : 0.9)) { best = c; best_st = st; }
+      if (c < best * (policy >= 2 ? 1.0 : 0.9)) { best = c; best_st = st; }
     }
     // hints.variant = v > 0: the v-th best distinct split the searches scored instead
     // (the profiler auto-tunes the physical plan of the best candidates over variants)
@@ -1488,6 +1494,38 @@ struct Gen {
     return (int)peak;
   }
 
+  // Loop-body loaders prefetched one iteration ahead into registers (TilePf):
+  // j-dependent plain tile loads of at most 8 loads per thread, 32 registers in all.
+  std::vector<char> pf;
+  void plan_prefetch() {
+    pf.assign(nodes.size(), 0);
+    if (getenv("SGM_NO_PREFETCH") || d.hints.no_prefetch || loop_begin_pos < 0 || nloop / LP < 2) return;
+    int regs = 0;
+    for (int p = loop_begin_pos; p < loop_end_pos; ++p) {
+      const Ev& e = sched[p];
+      if (e.type != Ev::NODE) continue;
+      const Node& x = nodes[e.node];
+      if (x.kind != SGM_INPUT || !x.body || x.hoist || !x.loopdep || x.inv || x.staged || x.store == ST_VIEW ||
+          x.store == ST_XG || e.node == ilv_big)
+        continue;
+      const int vec = io_vec(x, true);
+      const i64 tot = prod4(x.sl) / (vec > 1 ? vec : 1);
+      const i64 it = (tot + NT - 1) / NT;
+      const int r = (int)it * (vec > 1 ? 4 : (es + 3) / 4);
+      if (it > 8 || regs + r > 32) continue;
+      regs += r;
+      pf[e.node] = 1;
+    }
+  }
+
+  std::string pf_type(const Node& x) const {
+    const i64* st = in_strides[x.slot];
+    std::ostringstream t;
+    t << "sgm::TilePf<N, " << x.sl[0] << ", " << x.sl[1] << ", " << x.sl[2] << ", " << x.sl[3] << ", " << st[0]
+      << "LL, " << st[1] << "LL, " << st[2] << "LL, " << st[3] << "LL, " << io_vec(x, true) << ", NT>";
+    return t.str();
+  }
+
   void plan_xcache() {
     for (auto& x : nodes) x.xc = false;
     xcache = xcache_loop = false;
@@ -2119,6 +2157,12 @@ struct Gen {
           os << "    sgm::csync<NT>();\n    if (tid == 0) sgm::mbar_arrive(&sempty[" << x.stage_id << "]);\n";
           return;
         }
+        if (in_loop && !pf.empty() && pf[n]) {  // this iteration's tile from registers, the next one's loads issued
+          os << "    pf" << n << ".store(" << tile_ptr(n) << ");\n";
+          os << "    if (j + 1 < (jp + 1) * " << nloop / LP << ") pf" << n << ".load((const S*)a.in[" << x.slot << "] + ("
+             << offset_expr(x, true, "(j + 1)") << "));\n";
+          break;
+        }
         std::string off = offset_expr(x, true, J);
         const i64* st = in_strides[x.slot];
         os << "    sgm::load_tile<N, " << x.sl[0] << ", " << x.sl[1] << ", " << x.sl[2] << ", " << x.sl[3] << ", "
@@ -2263,6 +2307,7 @@ struct Gen {
   }
 
   void emit() {
+    plan_prefetch();
     if (d.hints.no_wd) os << "#define SGM_WD_MODE 0  // canonical unbounded waits (no watchdog)\n";
     os << "#include \"sgm_dev.cuh\"\n";
     os << "// generated by sgm_codegen.cpp: logical blocks " << LB << ", free parts " << FP << ", cluster " << CL
@@ -2412,6 +2457,10 @@ struct Gen {
         // consecutive tiles are adjacent in memory, so a strided column tile's
         // sectors serve the next iterations from L1/L2 (interleaved parts re-fetched
         // every sector; A's split-KV candidates read Kt one column per iteration)
+        for (int n = 0; n < (int)pf.size(); ++n)
+          if (pf[n])
+            os << "  " << pf_type(nodes[n]) << " pf" << n << ";\n  pf" << n << ".load((const S*)a.in[" << nodes[n].slot
+               << "] + (" << offset_expr(nodes[n], true, "(jp * " + std::to_string(nloop / LP) + ")") << "));\n";
         os << "  for (int j = jp * " << nloop / LP << "; j < (jp + 1) * " << nloop / LP << "; ++j) {\n";
         in_loop = true;
       } else if (e.type == Ev::LOOP_END) {

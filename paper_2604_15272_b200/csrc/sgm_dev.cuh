@@ -250,6 +250,54 @@ __device__ __forceinline__ uint2 ldg_stream8(const void* p) {
 // Tile movement: strided rank-4 global view <-> dense smem tile.
 // VEC > 1 only when the planner proved 16-byte alignment of every row start.
 
+// Register prefetch of a small loop-body tile (at most 8 loads per thread): the
+// next iteration's global loads are issued right after this iteration's tile is
+// written to shared memory, so their latency hides behind the rest of the
+// iteration instead of opening it (A's split-KV loops: one Kt column and one V
+// row per key, two dependent round trips per iteration otherwise).
+template <class N, int D0, int D1, int D2, int D3, i64 S0, i64 S1, i64 S2, i64 S3, int VEC, int NT>
+struct TilePf {
+  typedef typename N::S S;
+  static constexpr int ROWS = D0 * D1 * D2;
+  static constexpr int V3 = VEC > 1 ? D3 / VEC : D3;
+  static constexpr int TOT = ROWS * V3;
+  static constexpr int IT = (TOT + NT - 1) / NT;
+  union U { uint4 q; S s[VEC > 1 ? VEC : 1]; };
+  U u[VEC > 1 ? IT : 1];
+  S r[VEC > 1 ? 1 : IT];
+
+  __device__ __forceinline__ void load(const S* __restrict__ src) {
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const int e = threadIdx.x + j * NT;
+      if (e < TOT) {
+        const int v = e % V3;
+        const int rr = e / V3;
+        const int i2 = rr % D2, i1 = (rr / D2) % D1, i0 = rr / (D2 * D1);
+        if constexpr (VEC > 1)
+          u[j].q = *reinterpret_cast<const uint4*>(src + i0 * S0 + i1 * S1 + i2 * S2 + (i64)v * VEC);
+        else
+          r[j] = src[i0 * S0 + i1 * S1 + i2 * S2 + (i64)v * S3];
+      }
+    }
+  }
+  __device__ __forceinline__ void store(typename N::C* __restrict__ dst) const {
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const int e = threadIdx.x + j * NT;
+      if (e < TOT) {
+        if constexpr (VEC > 1) {
+          const int v = e % V3, rr = e / V3;
+#pragma unroll
+          for (int t = 0; t < VEC; ++t) dst[rr * D3 + v * VEC + t] = N::ld(u[j].s[t]);
+        } else {
+          dst[e] = N::ld(r[j]);
+        }
+      }
+    }
+  }
+};
+
 template <class N, int D0, int D1, int D2, int D3, i64 S0, i64 S1, i64 S2, i64 S3, int VEC, int NT>
 __device__ __forceinline__ void load_tile(typename N::C* __restrict__ dst, const typename N::S* __restrict__ src) {
   typedef typename N::S S;

@@ -139,6 +139,7 @@ def build_desc(c: Candidate, numsys: int, hints: Optional[dict] = None) -> _abi.
     d.hints.interleave = int(h.get("interleave", 0))
     d.hints.ff_tma = int(h.get("ff_tma", 0))
     d.hints.no_xcache = int(h.get("no_xcache", 0))
+    d.hints.no_prefetch = int(h.get("no_prefetch", 0))
     return d
 
 

@@ -116,3 +116,37 @@ def test_x_cache_is_exact(S, w, mapping, x):
     ref = block_np.run_program(progd, ins_d)
     got = S.run_concrete(u.cand, ins_d, dtype=dt)
     assert S.rel_err(got["O"], ref["O"]) < 1e-2, (w, x)
+
+
+@pytest.mark.parametrize("w,mapping,params", [
+    ("A", "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 16, "i": 2048}),
+    ("A", "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 1, "i": 8192}),
+    ("L", "A.0.i,B.1.x,O.1.x,W.0.i,W.1.x,X.1.i", {"x": 256, "i": 2048}),
+])
+def test_loop_prefetch_is_exact(S, w, mapping, params):
+    """Loop-body tiles prefetched into registers one iteration ahead (TilePf):
+    FF bit-exact against the program with and without the prefetch, the
+    deployment dtype against the fp64 oracle."""
+    import torch
+    from oracle import block_np
+    from paper_2604_15272_b200 import population as P
+    from paper_2604_15272_b200.ff import ff_fill_inputs, ff_run, ff_trial_seed
+    pop = P.load_population(w)
+    u = next(v for v in P.units(pop) if v.cand.mapping_list() == sorted(mapping.split(",")) and v.cand.params == params)
+    prog = u.cand.program
+    ins = ff_fill_inputs(prog, ff_trial_seed(11, 2, 0), 0)
+    exp = ff_run(S.ir.program_candidate(prog), ins, 0)
+    for hints in (None, {"no_prefetch": 1}):
+        plan = S.Plan(u.cand, 3, hints, 0)
+        assert ("TilePf" in plan.source()) == (hints is None)
+        for _ in range(2):
+            outs = [torch.empty_like(e) for e in exp]
+            plan.run(ins, outs)
+            assert all(torch.equal(a, b) for a, b in zip(outs, exp)), (w, params, hints)
+    rng = np.random.default_rng(37)
+    progd = pop["program"]
+    ins_d = {t["name"]: torch.from_numpy(rng.standard_normal(tuple(t["dims"]))).bfloat16().double().numpy()
+             for t in progd["tensors"] if t["role"] == "input"}
+    ref = block_np.run_program(progd, ins_d)
+    got = S.run_concrete(u.cand, ins_d, dtype=pop["dtype"])
+    assert S.rel_err(got["O"], ref["O"]) < 1e-2, (w, params)
