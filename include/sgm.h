@@ -209,7 +209,8 @@ int sgm_plan_cubin(const sgm_plan* plan, void* buf, size_t cap, size_t* len);
 int sgm_plan_destroy(sgm_plan* plan);
 
 /* Outputs are first filled with NaN (fp) / 0xFFFFFFFF (FF) when init_outputs != 0,
- * reproducing the reference's NaN-initialised outputs (interp.py:147-152). */
+ * reproducing the reference's NaN-initialised outputs (interp.py:147-152).
+ * Every input and output pointer must be 16-byte aligned (SGM_ERR_INVALID otherwise). */
 int sgm_plan_run(sgm_plan* plan, const void* const* inputs, void* const* outputs,
                  int init_outputs, void* stream);
 /* Timeline of the last run of a plan created with hints.trace = 1: for every

@@ -699,6 +699,9 @@ struct Gen {
     const double base = d.hints.item_cost_ns > 0 ? d.hints.item_cost_ns * 1e-9 : 4.0e-6;
     double t_item = (base + cflush * 5.0e-6 + gflush * 2.0e-6 * (base / 4.0e-6)) * (two ? 0.4 : 1.0);
     double loop_iters = loop_begin_pos >= 0 ? (double)nloop / LP : 0.0;
+    // an x-cached loop runs only when a CTA's item moves to other coordinates
+    if (xcache && xcache_loop)
+      loop_iters *= std::min(1.0, ((double)items / (double)grid[0] + (double)active) / (double)items);
     t_item += loop_iters * 0.6e-6;
     return t_stream + (double)rounds * t_item + over;
   }
@@ -1508,14 +1511,47 @@ struct Gen {
       if (x.kind != SGM_INPUT || !x.body || x.hoist || !x.loopdep || x.inv || x.staged || x.store == ST_VIEW ||
           x.store == ST_XG || e.node == ilv_big)
         continue;
+      if (strip_ok(x)) {
+        const i64 it = (x.sl[0] * x.sl[1] * x.sl[2] + NT - 1) / NT;
+        if (it <= 8 && regs + 4 * it <= 40) {
+          regs += 4 * (int)it;
+          pf[e.node] = 2;
+          continue;
+        }
+      }
       const int vec = io_vec(x, true);
       const i64 tot = prod4(x.sl) / (vec > 1 ? vec : 1);
       const i64 it = (tot + NT - 1) / NT;
       const int r = (int)it * (vec > 1 ? 4 : (es + 3) / 4);
-      if (it > 8 || regs + r > 32) continue;
+      if (it > 8 || regs + r > 40) continue;
       regs += r;
       pf[e.node] = 1;
     }
+  }
+
+  // A loader whose loop steps its contiguous innermost dim T elements per iteration
+  // with a T-element tile along it (T columns per iteration, T | 16 / es): TileStrip
+  // reads the next 16 bytes of every row once per 16 / es / T iterations.  Every other offset term
+  // must keep 16-byte alignment (sgm_plan_run requires 16-byte aligned base pointers).
+  bool strip_ok(const Node& x) const {
+    if (getenv("SGM_NO_STRIP")) return false;
+    const i64 G = 16 / es;
+    const i64* dims = in_dims[x.slot];
+    const i64* st = in_strides[x.slot];
+    const i64 T = x.sl[3];
+    if (G % T || st[3] != 1 || !x.lsplit[3] || (nloop / LP) % (G / T)) return false;
+    i64 w = dims[3];
+    for (int g = 0; g < ngrid; ++g)
+      if (x.gmask[3] >> g & 1u) {
+        w /= grid[g];
+        if (grid[g] > 1 && w % G) return false;
+      }
+    if (w / nloop != T) return false;
+    const int c = x.cls[3];
+    if (c >= 0 && cls[c].parts > 1 && (x.sh[3] / cls[c].parts) % G) return false;
+    for (int k = 0; k < 3; ++k)
+      if (dims[k] > 1 && st[k] % G) return false;
+    return true;
   }
 
   std::string pf_type(const Node& x) const {
@@ -1524,6 +1560,32 @@ struct Gen {
     t << "sgm::TilePf<N, " << x.sl[0] << ", " << x.sl[1] << ", " << x.sl[2] << ", " << x.sl[3] << ", " << st[0]
       << "LL, " << st[1] << "LL, " << st[2] << "LL, " << st[3] << "LL, " << io_vec(x, true) << ", NT>";
     return t.str();
+  }
+
+  bool any_tc() const {
+    for (auto& x : nodes)
+      if (x.kind == SGM_MATMUL && x.tc) return true;
+    return false;
+  }
+
+  // Loops over small tiles (L's one-k-per-iteration LoRA candidates: every body tile
+  // <= 128 elements, 4096 iterations) are barrier-latency chains; 256 threads leave
+  // most lanes idle and cap residency (registers).  Fewer threads per CTA -- at least
+  // a quarter of the largest body tile, a 64th of the largest other tile -- put more
+  // CTAs (independent chains) on each SM.  CUDA-core plans without a producer only.
+  int small_loop_threads() const {
+    if (d.hints.threads > 0 || prod || CL > 1 || any_tc() || getenv("SGM_NO_SMALL_NT")) return 0;
+    if (loop_begin_pos < 0 || nloop / LP < 16) return 0;
+    i64 wb = 0, wa = 0;
+    for (auto& x : nodes) {
+      if (x.store == ST_VIEW || x.store == ST_XG || x.kind == SGM_OUTPUT) continue;
+      const i64 w = prod4(x.sl);
+      if (x.body && !x.hoist) wb = std::max(wb, w);
+      else wa = std::max(wa, w);
+    }
+    int nt = 32;
+    while (nt < NT && (nt * 4 < wb || nt * 64 < wa)) nt *= 2;
+    return nt < NT ? nt : 0;
   }
 
   void plan_xcache() {
@@ -2157,7 +2219,16 @@ struct Gen {
           os << "    sgm::csync<NT>();\n    if (tid == 0) sgm::mbar_arrive(&sempty[" << x.stage_id << "]);\n";
           return;
         }
-        if (in_loop && !pf.empty() && pf[n]) {  // this iteration's tile from registers, the next one's loads issued
+        if (in_loop && !pf.empty() && pf[n] == 2) {  // column strip: a 16-byte load per row every G iterations
+          const i64 G = 16 / es / x.sl[3];  // iterations per strip
+          const std::string j0 = "(jp * " + std::to_string(nloop / LP) + ")";
+          // the next strip is loaded right after the last column of this one is written
+          os << "    st" << n << ".store(" << tile_ptr(n) << ", (j - " << j0 << ") & " << G - 1 << ");\n";
+          os << "    if (((j - " << j0 << ") & " << G - 1 << ") == " << G - 1 << " && j + 1 < (jp + 1) * " << nloop / LP
+             << ") st" << n << ".load((const S*)a.in[" << x.slot << "] + (" << offset_expr(x, true, "(j + 1)") << "));\n";
+          break;
+        }
+        if (in_loop && !pf.empty() && pf[n] == 1) {  // this iteration's tile from registers, the next one's loads issued
           os << "    pf" << n << ".store(" << tile_ptr(n) << ");\n";
           os << "    if (j + 1 < (jp + 1) * " << nloop / LP << ") pf" << n << ".load((const S*)a.in[" << x.slot << "] + ("
              << offset_expr(x, true, "(j + 1)") << "));\n";
@@ -2457,10 +2528,19 @@ struct Gen {
         // consecutive tiles are adjacent in memory, so a strided column tile's
         // sectors serve the next iterations from L1/L2 (interleaved parts re-fetched
         // every sector; A's split-KV candidates read Kt one column per iteration)
-        for (int n = 0; n < (int)pf.size(); ++n)
-          if (pf[n])
-            os << "  " << pf_type(nodes[n]) << " pf" << n << ";\n  pf" << n << ".load((const S*)a.in[" << nodes[n].slot
-               << "] + (" << offset_expr(nodes[n], true, "(jp * " + std::to_string(nloop / LP) + ")") << "));\n";
+        for (int n = 0; n < (int)pf.size(); ++n) {
+          const Node& x = nodes[n];
+          if (pf[n] == 1)
+            os << "  " << pf_type(x) << " pf" << n << ";\n  pf" << n << ".load((const S*)a.in[" << x.slot << "] + ("
+               << offset_expr(x, true, "(jp * " + std::to_string(nloop / LP) + ")") << "));\n";
+          if (pf[n] == 2) {
+            const i64* st = in_strides[x.slot];
+            os << "  sgm::TileStrip<N, " << x.sl[0] << ", " << x.sl[1] << ", " << x.sl[2] << ", " << x.sl[3] << ", "
+               << st[0] << "LL, "
+               << st[1] << "LL, " << st[2] << "LL, NT> st" << n << ";\n  st" << n << ".load((const S*)a.in["
+               << x.slot << "] + (" << offset_expr(x, true, "(jp * " + std::to_string(nloop / LP) + ")") << "));\n";
+          }
+        }
         os << "  for (int j = jp * " << nloop / LP << "; j < (jp + 1) * " << nloop / LP << "; ++j) {\n";
         in_loop = true;
       } else if (e.type == Ev::LOOP_END) {
@@ -2585,6 +2665,23 @@ struct Gen {
       no_tma_forced = true;
       ok = fit();
     }
+    if (const int nt = small_loop_threads()) {  // re-plan with fewer threads per CTA
+      const int keep = NT;
+      const bool keep_forced = no_tma_forced;
+      NT = nt;
+      split_plan();
+      ok = fit();
+      if (!ok || prod || any_tc()) {
+        NT = keep;
+        no_tma_forced = keep_forced;
+        split_plan();
+        ok = fit();
+        if (!ok && prod) {
+          no_tma_forced = true;
+          ok = fit();
+        }
+      }
+    }
     plan_ring();
     plan_interleave();
     plan_accfuse();
@@ -2671,6 +2768,7 @@ struct Gen {
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) R.n_tcgen05++;
     std::ostringstream s;
+    if (NT != 256) s << "NT=" << NT << " ";
     s << "LB=" << LB << " FP=" << FP << " GP=" << GP << " CL=" << CL << " LP=" << LP << (loop_gs ? "g" : "")
       << " ring=" << ringS << "x" << slotB / 1024 << "K est=" << (int)est_us << "us smem=" << smem_peak
       << " scratch/cta=" << scratch_per_cta << " classes:";

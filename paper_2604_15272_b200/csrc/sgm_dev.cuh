@@ -255,6 +255,57 @@ __device__ __forceinline__ uint2 ldg_stream8(const void* p) {
 // written to shared memory, so their latency hides behind the rest of the
 // iteration instead of opening it (A's split-KV loops: one Kt column and one V
 // row per key, two dependent round trips per iteration otherwise).
+// Element e of a 16-byte vector as the storage type (selects, no local memory).
+template <class S> __device__ __forceinline__ S vec_pick(const uint4& q, int e);
+template <> __device__ __forceinline__ u16 vec_pick<u16>(const uint4& q, int e) {
+  const u32 w = (e & 4) ? ((e & 2) ? q.w : q.z) : ((e & 2) ? q.y : q.x);
+  return (u16)((e & 1) ? (w >> 16) : (w & 0xffffu));
+}
+template <> __device__ __forceinline__ u32 vec_pick<u32>(const uint4& q, int e) {
+  return (e & 2) ? ((e & 1) ? q.w : q.z) : ((e & 1) ? q.y : q.x);
+}
+template <> __device__ __forceinline__ float vec_pick<float>(const uint4& q, int e) {
+  return __uint_as_float(vec_pick<u32>(q, e));
+}
+template <> __device__ __forceinline__ double vec_pick<double>(const uint4& q, int e) {
+  return e ? __hiloint2double((int)q.w, (int)q.z) : __hiloint2double((int)q.y, (int)q.x);
+}
+
+// Column strip of a loop that steps a contiguous innermost dim T elements per
+// iteration (A's Kt.3.i: one key column [.., 128, 1] per iteration, every element
+// in its own sector): each lane loads 16 bytes of its rows -- the next G / T
+// iterations' columns, G = 16 / sizeof(S) -- once per G / T iterations, and every
+// iteration writes its columns from registers.  G / T-fold fewer L1 wavefronts.
+template <class N, int D0, int D1, int D2, int T, i64 S0, i64 S1, i64 S2, int NT>
+struct TileStrip {
+  typedef typename N::S S;
+  static constexpr int ROWS = D0 * D1 * D2;
+  static constexpr int IT = (ROWS + NT - 1) / NT;
+  uint4 u[IT];
+
+  __device__ __forceinline__ void load(const S* __restrict__ src) {
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const int r = threadIdx.x + j * NT;
+      if (r < ROWS) {
+        const int i2 = r % D2, i1 = (r / D2) % D1, i0 = r / (D2 * D1);
+        u[j] = *reinterpret_cast<const uint4*>(src + i0 * S0 + i1 * S1 + i2 * S2);
+      }
+    }
+  }
+  // iteration e of the strip: its T consecutive elements of every row
+  __device__ __forceinline__ void store(typename N::C* __restrict__ dst, int e) const {
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const int r = threadIdx.x + j * NT;
+      if (r < ROWS) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) dst[r * T + t] = N::ld(vec_pick<S>(u[j], e * T + t));
+      }
+    }
+  }
+};
+
 template <class N, int D0, int D1, int D2, int D3, i64 S0, i64 S1, i64 S2, i64 S3, int VEC, int NT>
 struct TilePf {
   typedef typename N::S S;
@@ -445,11 +496,49 @@ __device__ __forceinline__ void sum_axis(typename N::C* __restrict__ dst, const 
 // A and B are either smem tiles (TA/TB = N::C) or global views (N::S), given by
 // compile-time strides (0 for broadcast dims).  TPO lanes split k.
 
+__host__ __device__ constexpr int pow2_divisor(int m, int cap) {
+  int r = 1;
+  while (r * 2 <= cap && m % (r * 2) == 0) r *= 2;
+  return r;
+}
+__host__ __device__ constexpr int divisor_upto(int m, int cap) {
+  int r = cap < m ? cap : m;
+  while (m % r) --r;
+  return r;
+}
+
+// Multi-value warp reduction: R (power of two) partial sums per lane in, the full
+// sum of value ((lane&16)?R/2:0) + ((lane&8)?R/4:0) + ... out -- R/2 + R/4 + ...
+// + the remaining single levels shuffles instead of 5 R.
+template <class N, int R>
+__device__ __forceinline__ typename N::A warp_reduce_multi(typename N::A (&v)[R], int lane) {
+  typedef typename N::A Acc;
+#pragma unroll
+  for (int lvl = 0; lvl < 5; ++lvl) {
+    const int off = 16 >> lvl;
+    const int r = R >> lvl;
+    if (r > 1) {
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < r / 2; ++i) {
+        const Acc send = up ? v[i] : v[i + r / 2];
+        Acc keep = up ? v[i + r / 2] : v[i];
+        N::amerge(keep, shfl_xor(send, off, 0xffffffffu));
+        v[i] = keep;
+      }
+    } else {
+      N::amerge(v[0], shfl_xor(v[0], off, 0xffffffffu));
+    }
+  }
+  return v[0];
+}
+
 template <class N, class TA, class TB, int B0, int B1, int M, int K, int NN,
           i64 SA0, i64 SA1, i64 SA2, i64 SA3, i64 SB0, i64 SB1, i64 SB2, i64 SB3, int NT>
 __device__ __forceinline__ void mm_generic(typename N::C* __restrict__ out, const TA* __restrict__ A,
                                            const TB* __restrict__ B) {
   typedef typename N::A Acc;
+  typedef typename N::C C;
   constexpr int OUT = B0 * B1 * M * NN;
   constexpr int TPO0 = pow2_floor(NT / OUT > 0 ? NT / OUT : 1);
   constexpr int TPO1 = TPO0 > 32 ? 32 : TPO0;
@@ -458,6 +547,64 @@ __device__ __forceinline__ void mm_generic(typename N::C* __restrict__ out, cons
   // output, lanes of different rows hit one bank (row stride a multiple of 32
   // words): A's Q @ Kt-column step took 12.7 us per loop iteration.
   constexpr bool DOT = SA3 == 1 && SB2 == 1 && K >= 32;
+  // smem operands, K a multiple of 32: a warp takes R rows sharing one B column
+  // (B contiguous along k) or all NB = NN columns of a row-major B tile (k stride
+  // NN <= 4, e.g. A's two keys per iteration), the k values held in registers
+  // (chunks of up to 8 per lane) and reused by all R rows, one multi-value
+  // reduction for the R x NB sums (A's Q @ Kt-column loop step: 7.8 us as a
+  // warp-per-output loop of 4 products and 5 shuffles each)
+  constexpr bool ROWB = SA3 == 1 && SB3 == 1 && SB2 == NN && NN > 1 && NN <= 4 && (NN & (NN - 1)) == 0;
+  if constexpr ((DOT || ROWB) && K % 32 == 0 && same_t<TA, C>::v && same_t<TB, C>::v) {
+    constexpr int NB = DOT ? 1 : NN;
+    constexpr int R = pow2_divisor(M, 8 / NB);
+    constexpr int V = R * NB;
+    constexpr int KS = K / 32;
+    constexpr int KC = divisor_upto(KS, 8 / NB);
+    constexpr int TASKS = B0 * B1 * (NN / NB) * (M / R);
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int t = tid >> 5; t < TASKS; t += NT / 32) {
+      int r = t;
+      const int mg = r % (M / R); r /= (M / R);
+      const int n0 = (r % (NN / NB)) * NB; r /= (NN / NB);
+      const int b1 = r % B1, b0 = r / B1;
+      const C* pa = A + b0 * SA0 + b1 * SA1 + (i64)(mg * R) * SA2 + lane;
+      const C* pb = B + b0 * SB0 + b1 * SB1 + (i64)n0 * SB3 + (i64)lane * SB2;
+      Acc v[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = N::azero();
+      for (int c = 0; c < KS; c += KC) {
+        C bv[KC][NB];
+#pragma unroll
+        for (int s = 0; s < KC; ++s)
+#pragma unroll
+          for (int q = 0; q < NB; ++q) bv[s][q] = pb[(i64)(c + s) * 32 * SB2 + q];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+#pragma unroll
+          for (int s = 0; s < KC; ++s) {
+            const C av = pa[(i64)i * SA2 + (c + s) * 32];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+              if constexpr (has_fold<N>::v) {
+                N::mac_raw(v[i * NB + q], av, bv[s][q]);
+                if (s % 3 == 2 || s == KC - 1) N::fold(v[i * NB + q]);
+              } else {
+                N::mac(v[i * NB + q], av, bv[s][q]);
+              }
+            }
+          }
+        }
+      }
+      const Acc tot = warp_reduce_multi<N, V>(v, lane);
+      if ((lane & (32 / V - 1)) == 0) {
+        int idx = 0;
+#pragma unroll
+        for (int lvl = 0; (V >> (lvl + 1)) > 0; ++lvl) idx += ((lane >> (4 - lvl)) & 1) * (V >> (lvl + 1));
+        out[(((i64)b0 * B1 + b1) * M + mg * R + idx / NB) * NN + n0 + idx % NB] = N::fin(tot);
+      }
+    }
+    return;
+  }
   constexpr int TPO2 = DOT ? 32 : TPO1;
   constexpr int TPO = TPO2 > pow2_ceil(K) ? pow2_ceil(K) : TPO2;
   constexpr int GROUPS = NT / TPO;

@@ -678,6 +678,12 @@ static int encode_tmap(sgm_plan* p, int i, const void* ptr) {
 }
 
 static int launch_plan(sgm_plan* p, const void* const* inputs, void* const* outputs, CUstream s) {
+  // generated kernels move rows with 16-byte vectors wherever the strides allow
+  // (and column strips, TMA boxes): every tensor base must be 16-byte aligned
+  for (int k = 0; k < p->n_in; ++k)
+    if ((uintptr_t)inputs[k] & 15) return set_err(SGM_ERR_INVALID, "input %d is not 16-byte aligned", k);
+  for (int k = 0; k < p->n_out; ++k)
+    if ((uintptr_t)outputs[k] & 15) return set_err(SGM_ERR_INVALID, "output %d is not 16-byte aligned", k);
   sgm::Args args;
   memset(&args, 0, sizeof args);
   for (int i = 0; i < (int)p->gen.tmaps.size() && i < 4; ++i) {

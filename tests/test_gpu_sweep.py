@@ -120,6 +120,7 @@ def test_x_cache_is_exact(S, w, mapping, x):
 
 @pytest.mark.parametrize("w,mapping,params", [
     ("A", "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 16, "i": 2048}),
+    ("A", "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 16, "i": 4096}),
     ("A", "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 1, "i": 8192}),
     ("L", "A.0.i,B.1.x,O.1.x,W.0.i,W.1.x,X.1.i", {"x": 256, "i": 2048}),
 ])
@@ -138,11 +139,18 @@ def test_loop_prefetch_is_exact(S, w, mapping, params):
     exp = ff_run(S.ir.program_candidate(prog), ins, 0)
     for hints in (None, {"no_prefetch": 1}):
         plan = S.Plan(u.cand, 3, hints, 0)
-        assert ("TilePf" in plan.source()) == (hints is None)
+        src = plan.source()
+        assert ("TilePf" in src or "TileStrip" in src) == (hints is None)
+        if w == "A" and hints is None:
+            assert "TileStrip" in src  # Kt's columns per key come from 16-byte row strips
         for _ in range(2):
             outs = [torch.empty_like(e) for e in exp]
             plan.run(ins, outs)
             assert all(torch.equal(a, b) for a, b in zip(outs, exp)), (w, params, hints)
+    # the generated kernels assume 16-byte aligned bases: a misaligned one is refused
+    buf = torch.empty(ins[0].numel() + 1, dtype=ins[0].dtype, device=ins[0].device)
+    with pytest.raises(ValueError, match="16-byte aligned"):
+        S.Plan(u.cand, 3, None, 0).run([buf[1:].view(ins[0].shape)] + list(ins[1:]), outs)
     rng = np.random.default_rng(37)
     progd = pop["program"]
     ins_d = {t["name"]: torch.from_numpy(rng.standard_normal(tuple(t["dims"]))).bfloat16().double().numpy()
