@@ -194,6 +194,10 @@ struct Gen {
   // read-back of its own), so acc_second's read-back is acc_first + acc_second and
   // the add node acc_add becomes a copy (LoRA: O = X@W + (X@A)@B)
   int acc_first = -1, acc_second = -1, acc_add = -1, acc_pre = 0;
+  // tcgen05 streams scheduled between the pair (hints.big_first: X@W, then X@A,
+  // then T@B into X@W's accumulators) use TMEM columns from acc_mid_off
+  std::set<int> acc_mids;
+  int acc_mid_off = 0;
   // finite field: a broadcast divisor tile consumed only by one div is inverted in
   // place once (Fermat inverse, ~60 modular products) and the div becomes a mul,
   // instead of one inverse per numerator element (QK-norm's [128, L] / [1, L])
@@ -699,9 +703,14 @@ struct Gen {
     const double base = d.hints.item_cost_ns > 0 ? d.hints.item_cost_ns * 1e-9 : 4.0e-6;
     double t_item = (base + cflush * 5.0e-6 + gflush * 2.0e-6 * (base / 4.0e-6)) * (two ? 0.4 : 1.0);
     double loop_iters = loop_begin_pos >= 0 ? (double)nloop / LP : 0.0;
-    // an x-cached loop runs only when a CTA's item moves to other coordinates
-    if (xcache && xcache_loop)
-      loop_iters *= std::min(1.0, ((double)items / (double)grid[0] + (double)active) / (double)items);
+    // x-cached work runs only when a CTA's item moves to other coordinates: the
+    // loop, and (a guess, without a compute term in this model) half of the
+    // fixed per-item work, which the cached matmuls dominate
+    if (xcache) {
+      const double miss = std::min(1.0, ((double)items / (double)grid[0] + (double)active) / (double)items);
+      if (xcache_loop) loop_iters *= miss;
+      t_item *= miss + 0.5 * (1.0 - miss);
+    }
     t_item += loop_iters * 0.6e-6;
     return t_stream + (double)rounds * t_item + over;
   }
@@ -1685,15 +1694,29 @@ struct Gen {
         Class& B = cls[bestc];
         const bool was_c = B.cluster, was_g = B.gsplit;
         B.parts *= 2;
+        // a new reduction split: gsplit when one is open already, or when the plan
+        // is x-cached (cluster plans cannot keep nodes across items), else cluster
+        const bool keep_xc = xcache && !getenv("SGM_NO_XC_FIT");
         if (B.reduced && B.parts == 2) {
-          if (GP > 1) B.gsplit = true;
+          if (GP > 1 || keep_xc) B.gsplit = true;
           else B.cluster = true;
         }
         finalize_layout();
         if (B.gsplit) {  // the reduction must still be a tail reduction
           slices();
           schedule();
-          if (!gs_tail_ok()) { B.parts /= 2; B.cluster = was_c; B.gsplit = was_g; finalize_layout(); bestc = -1; }
+          if (!gs_tail_ok()) {
+            B.gsplit = was_g;
+            if (B.reduced && B.parts == 2 && GP == 1 && keep_xc && CL * 2 <= max_cluster) {
+              B.cluster = true;  // no tail reduction: the cluster split after all
+              finalize_layout();
+            } else {
+              B.parts /= 2;
+              B.cluster = was_c;
+              finalize_layout();
+              bestc = -1;
+            }
+          }
         }
         if (bestc >= 0) continue;
       }
@@ -2117,6 +2140,8 @@ struct Gen {
 
   void plan_accfuse() {
     acc_first = acc_second = acc_add = -1;
+    acc_mids.clear();
+    acc_mid_off = 0;
     if (getenv("SGM_NO_ACCFUSE") || !prod || ilv_big >= 0) return;
     std::vector<int> pos(nodes.size(), -1);
     for (int p = 0; p < (int)sched.size(); ++p)
@@ -2135,13 +2160,32 @@ struct Gen {
       if (!ok(A) || !ok(B) || A.acc != B.acc || A.tc_cols != B.tc_cols || A.xc || B.xc) continue;
       if (pos[a] < 0 || pos[b] < 0) continue;
       int f = pos[a] < pos[b] ? a : b, sec = f == a ? b : a;
-      if (pos[sec] != pos[f] + 1 || pos[n] < pos[sec]) continue;  // adjacent, nothing in between
+      if (pos[n] < pos[sec]) continue;
+      // in between: nothing that touches TMEM except tcgen05 streams, which get
+      // their own columns after the pair's accumulators
+      bool mid_ok = true;
+      std::set<int> mids;
+      for (int p = pos[f] + 1; p < pos[sec] && mid_ok; ++p) {
+        if (sched[p].type != Ev::NODE) { mid_ok = false; break; }
+        const Node& y = nodes[sched[p].node];
+        if (y.kind != SGM_MATMUL) continue;
+        if (y.tma && y.tc && !y.inv && !y.body) mids.insert(sched[p].node);
+        else if (y.tc) mid_ok = false;
+      }
+      if (!mid_ok || (!mids.empty() && getenv("SGM_NO_ACCMID"))) continue;
       const Node& F = nodes[f];
+      int mc = 0;
+      for (int y : mids) mc = std::max(mc, nodes[y].tc_cols);
+      int tot = 32;
+      while (tot < F.tc_cols + mc) tot *= 2;
+      if (!mids.empty() && tot > (paired ? 256 : 512)) continue;
       const int nmma = (int)(nodes[F.in[0]].sl[3] / 16);
       acc_first = f;
       acc_second = sec;
       acc_add = n;
       acc_pre = std::min(F.acc, nmma);
+      acc_mids = mids;
+      acc_mid_off = F.tc_cols;
       return;
     }
   }
@@ -2323,7 +2367,9 @@ struct Gen {
                                        : ", " + std::to_string(ilv_kc) + ", " + std::to_string(K / x.kc) + ", true";
           if (n == acc_first) seg = ", 0, " + std::to_string(K / x.kc) + ", false";
           if (n == acc_second) seg = ", 0, " + std::to_string(K / x.kc) + ", true, " + std::to_string(acc_pre);
-          const std::string tm = chain_node ? "tmem_base + " + std::to_string(ilv_tmem) + "u" : std::string("tmem_base");
+          const std::string tm = chain_node ? "tmem_base + " + std::to_string(ilv_tmem) + "u"
+                                 : acc_mids.count(n) ? "tmem_base + " + std::to_string(acc_mid_off) + "u"
+                                                     : std::string("tmem_base");
           os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS << ", "
              << slotB << ", NT, " << (build ? "true" : "false") << ", " << x.acc << seg << ">(" << tile_ptr(n) << ", " << pa
@@ -2467,6 +2513,13 @@ struct Gen {
     int tmem_cols = 0;
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) tmem_cols = std::max(tmem_cols, x.tc_cols);
+    if (!acc_mids.empty()) {  // the accumulate-into pair's columns, then the streams between them
+      int c = 0;
+      for (int n : acc_mids) c = std::max(c, nodes[n].tc_cols);
+      int t = 32;
+      while (t < acc_mid_off + c) t *= 2;
+      tmem_cols = std::max(tmem_cols, t);
+    }
     if (ilv_big >= 0) {  // big-stream accumulators + the chain's, side by side
       int c = 0;
       for (int n : ilv_chain) c = std::max(c, nodes[n].tc_cols);

@@ -1219,6 +1219,7 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
   constexpr u32 IDESC = UMMA_IDESC_BF16_M128_N16;
   constexpr int NMMA = K / 16;                      // MMAs per tile
   constexpr int AC = ACC < NMMA ? ACC : NMMA;        // accumulators actually written
+  constexpr int AR = AC > PRE ? AC : PRE;            // accumulators read back (an earlier call's too)
   // narrow tile (NN <= 64): one 64-column box per stage; the MMA's second 64-row
   // half re-reads the first (LBO 0) and its results are discarded in the epilogue
   constexpr bool NARROW = NN <= 64;
@@ -1268,7 +1269,7 @@ __device__ __noinline__ void mm_stream_tc_core(float* __restrict__ out, const fl
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
 #pragma unroll
-      for (int a = 0; a < AC; ++a) {
+      for (int a = 0; a < AR; ++a) {
         u32 v[16];
         tmem_ld16(tmem + ((u32)((warp & 3) * 32) << 16) + (t * ACC + a) * 16, v);
 #pragma unroll
