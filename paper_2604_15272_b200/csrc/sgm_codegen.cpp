@@ -194,10 +194,6 @@ struct Gen {
   // read-back of its own), so acc_second's read-back is acc_first + acc_second and
   // the add node acc_add becomes a copy (LoRA: O = X@W + (X@A)@B)
   int acc_first = -1, acc_second = -1, acc_add = -1, acc_pre = 0;
-  // tcgen05 streams scheduled between the pair (hints.big_first: X@W, then X@A,
-  // then T@B into X@W's accumulators) use TMEM columns from acc_mid_off
-  std::set<int> acc_mids;
-  int acc_mid_off = 0;
   // finite field: a broadcast divisor tile consumed only by one div is inverted in
   // place once (Fermat inverse, ~60 modular products) and the div becomes a mul,
   // instead of one inverse per numerator element (QK-norm's [128, L] / [1, L])
@@ -2140,8 +2136,6 @@ struct Gen {
 
   void plan_accfuse() {
     acc_first = acc_second = acc_add = -1;
-    acc_mids.clear();
-    acc_mid_off = 0;
     if (getenv("SGM_NO_ACCFUSE") || !prod || ilv_big >= 0) return;
     std::vector<int> pos(nodes.size(), -1);
     for (int p = 0; p < (int)sched.size(); ++p)
@@ -2160,32 +2154,15 @@ struct Gen {
       if (!ok(A) || !ok(B) || A.acc != B.acc || A.tc_cols != B.tc_cols || A.xc || B.xc) continue;
       if (pos[a] < 0 || pos[b] < 0) continue;
       int f = pos[a] < pos[b] ? a : b, sec = f == a ? b : a;
-      if (pos[n] < pos[sec]) continue;
-      // in between: nothing that touches TMEM except tcgen05 streams, which get
-      // their own columns after the pair's accumulators
-      bool mid_ok = true;
-      std::set<int> mids;
-      for (int p = pos[f] + 1; p < pos[sec] && mid_ok; ++p) {
-        if (sched[p].type != Ev::NODE) { mid_ok = false; break; }
-        const Node& y = nodes[sched[p].node];
-        if (y.kind != SGM_MATMUL) continue;
-        if (y.tma && y.tc && !y.inv && !y.body) mids.insert(sched[p].node);
-        else if (y.tc) mid_ok = false;
-      }
-      if (!mid_ok || (!mids.empty() && getenv("SGM_NO_ACCMID"))) continue;
+      // adjacent, nothing in between (measured: X@W first with X@A -> T@B in their own
+      // TMEM columns after it was 9% slower on L -- the chain's stream queues behind W)
+      if (pos[sec] != pos[f] + 1 || pos[n] < pos[sec]) continue;
       const Node& F = nodes[f];
-      int mc = 0;
-      for (int y : mids) mc = std::max(mc, nodes[y].tc_cols);
-      int tot = 32;
-      while (tot < F.tc_cols + mc) tot *= 2;
-      if (!mids.empty() && tot > (paired ? 256 : 512)) continue;
       const int nmma = (int)(nodes[F.in[0]].sl[3] / 16);
       acc_first = f;
       acc_second = sec;
       acc_add = n;
       acc_pre = std::min(F.acc, nmma);
-      acc_mids = mids;
-      acc_mid_off = F.tc_cols;
       return;
     }
   }
@@ -2367,9 +2344,7 @@ struct Gen {
                                        : ", " + std::to_string(ilv_kc) + ", " + std::to_string(K / x.kc) + ", true";
           if (n == acc_first) seg = ", 0, " + std::to_string(K / x.kc) + ", false";
           if (n == acc_second) seg = ", 0, " + std::to_string(K / x.kc) + ", true, " + std::to_string(acc_pre);
-          const std::string tm = chain_node ? "tmem_base + " + std::to_string(ilv_tmem) + "u"
-                                 : acc_mids.count(n) ? "tmem_base + " + std::to_string(acc_mid_off) + "u"
-                                                     : std::string("tmem_base");
+          const std::string tm = chain_node ? "tmem_base + " + std::to_string(ilv_tmem) + "u" : std::string("tmem_base");
           os << "    sgm::mm_stream_tc<" << x.sl[0] << ", " << x.sl[1] << ", " << M << ", " << K << ", " << NN << ", "
              << sa[0] << "LL, " << sa[1] << "LL, " << sa[2] << "LL, " << sa[3] << "LL, " << x.kc << ", " << ringS << ", "
              << slotB << ", NT, " << (build ? "true" : "false") << ", " << x.acc << seg << ">(" << tile_ptr(n) << ", " << pa
@@ -2513,13 +2488,6 @@ struct Gen {
     int tmem_cols = 0;
     for (auto& x : nodes)
       if (x.kind == SGM_MATMUL && x.gemv && x.tc) tmem_cols = std::max(tmem_cols, x.tc_cols);
-    if (!acc_mids.empty()) {  // the accumulate-into pair's columns, then the streams between them
-      int c = 0;
-      for (int n : acc_mids) c = std::max(c, nodes[n].tc_cols);
-      int t = 32;
-      while (t < acc_mid_off + c) t *= 2;
-      tmem_cols = std::max(tmem_cols, t);
-    }
     if (ilv_big >= 0) {  // big-stream accumulators + the chain's, side by side
       int c = 0;
       for (int n : ilv_chain) c = std::max(c, nodes[n].tc_cols);

@@ -178,8 +178,7 @@ def test_interleaved_stream_deployment_dtype(S, params, hints):
 
 
 @pytest.mark.parametrize("params", [{"x": 32, "i": 1}, {"x": 2, "i": 1}, {"x": 8, "i": 1}])
-@pytest.mark.parametrize("hints", [{"one_cta": 1}, {}, {"one_cta": 1, "slot_kb": 16, "no_wd": 1},
-                                   {"one_cta": 1, "big_first": 1}, {"one_cta": 1, "big_first": 1, "no_wd": 1}])
+@pytest.mark.parametrize("hints", [{"one_cta": 1}, {}, {"one_cta": 1, "slot_kb": 16, "no_wd": 1}])
 def test_accumulate_into_deployment_dtype(S, params, hints):
     """LoRA's T@B issued into X@W's TMEM accumulators (accumulate-into fusion: one
     read-back gives X@W + T@B, the add becomes a copy), bf16 vs the fp64 oracle."""
@@ -189,10 +188,7 @@ def test_accumulate_into_deployment_dtype(S, params, hints):
     u = next(x for x in P.units(pop) if x.cand.mapping_list() == ["B.1.x", "O.1.x", "W.1.x"]
              and x.cand.params == params and pop["candidates"][x.pair]["template_id"] == 4)
     src = S.Plan(u.cand, 2, hints or None, None).source()
-    if hints.get("big_first"):  # X@W without read-back, X@A in its own TMEM columns, T@B with PRE = 4
-        assert ", false>(t5" in src and "tmem_base + 64u" in src and "true, 4>(t6" in src
-    else:
-        assert ", false>(t" in src and "true, 1>(t" in src  # T@B without read-back, X@W with PRE = 1
+    assert ", false>(t" in src and "true, 1>(t" in src  # T@B without read-back, X@W with PRE = 1
     rng = np.random.default_rng(29)
     prog = pop["program"]
     ins = {t["name"]: _round(rng.standard_normal(tuple(t["dims"])), "bf16") for t in prog["tensors"]
