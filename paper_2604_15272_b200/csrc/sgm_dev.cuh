@@ -554,7 +554,11 @@ __device__ __forceinline__ void mm_generic(typename N::C* __restrict__ out, cons
   // reduction for the R x NB sums (A's Q @ Kt-column loop step: 7.8 us as a
   // warp-per-output loop of 4 products and 5 shuffles each)
   constexpr bool ROWB = SA3 == 1 && SB3 == 1 && SB2 == NN && NN > 1 && NN <= 4 && (NN & (NN - 1)) == 0;
+#ifdef SGM_NO_DOT2
+  if constexpr (false) {
+#else
   if constexpr ((DOT || ROWB) && K % 32 == 0 && same_t<TA, C>::v && same_t<TB, C>::v) {
+#endif
     constexpr int NB = DOT ? 1 : NN;
     constexpr int R = pow2_divisor(M, 8 / NB);
     constexpr int V = R * NB;
@@ -1502,17 +1506,27 @@ __device__ __forceinline__ void gws_reduce(typename N::C* __restrict__ t, const 
   typedef typename N::A Acc;
   constexpr int VW = 16 / sizeof(C);
   constexpr int NV = SZ / VW;
+  // partials in batches of up to 8 loads in flight per thread: all GP at once held
+  // GP x 16 bytes in registers (GP = 128: 512 registers, the whole kernel spilled
+  // and ran one CTA per SM for the sake of its tail)
+  constexpr int QB = GP < 8 ? GP : 8;
+  static_assert(GP % QB == 0, "gsplit parts are powers of two");
   for (int v = threadIdx.x; v < NV; v += NT) {
-    union U { uint4 q; C c[VW]; } u[GP];
+    Acc acc[VW];
 #pragma unroll
-    for (int q = 0; q < GP; ++q) u[q].q = __ldcg(reinterpret_cast<const uint4*>(gw + q * STRIDE) + v);
+    for (int i = 0; i < VW; ++i) acc[i] = N::azero();
+#pragma unroll 1
+    for (int q0 = 0; q0 < GP; q0 += QB) {
+      union U { uint4 q; C c[VW]; } u[QB];
 #pragma unroll
-    for (int i = 0; i < VW; ++i) {
-      Acc acc = N::azero();
+      for (int q = 0; q < QB; ++q) u[q].q = __ldcg(reinterpret_cast<const uint4*>(gw + (q0 + q) * STRIDE) + v);
 #pragma unroll
-      for (int q = 0; q < GP; ++q) N::aadd(acc, u[q].c[i]);
-      t[v * VW + i] = N::fin(acc);
+      for (int i = 0; i < VW; ++i)
+#pragma unroll
+        for (int q = 0; q < QB; ++q) N::aadd(acc[i], u[q].c[i]);
     }
+#pragma unroll
+    for (int i = 0; i < VW; ++i) t[v * VW + i] = N::fin(acc[i]);
   }
   for (int e = NV * VW + threadIdx.x; e < SZ; e += NT) {
     Acc acc = N::azero();

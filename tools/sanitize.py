@@ -8,7 +8,8 @@ deployment dtype and once in GF(p), for compute-sanitizer:
 Modes: gsplit tail reduction (global partials + self-resetting counters),
 cluster one-barrier push (small DSMEM partials), cluster reduce-scatter +
 all-gather (large partials), two TMEM-allocating CTAs per SM (paired tcgen05),
-fp32 TMA ring on CUDA cores.  Prints each plan summary and the max rel_err of
+fp32 TMA ring on CUDA cores; round 2's x-cache, column strips + register
+prefetch and small-tile thread counts.  Prints each plan summary and the max rel_err of
 the second launch against the first (launch-to-launch determinism).
 """
 import os
@@ -30,6 +31,11 @@ CASES = [
     ("cluster-rs-ag", "A", 42, "Kt.1.x,O.1.x,Q.1.x,V.1.x", {"x": 2, "i": 1}, {"max_cluster": 8, "max_gsplit": 1}),
     ("paired-tmem", "Q", 36, "Kt.0.x,O.0.x,Q.0.x,V.0.x", {"x": 8, "i": 1}, {}),
     ("f32-ring", "R", 26, "O.1.x,W.1.x", {"x": 2, "i": 1}, {"one_cta": 1, "max_cluster": 1}),
+    # round 2 codegen: x-cache, column strips (T = 1, 2) + register prefetch, small-tile thread count
+    ("x-cache", "A", 57, "Kt.2.i,O.3.x,Q.3.i,V.3.x", {"x": 16, "i": 1}, {}),
+    ("strip-1", "A", 38, "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 2, "i": 8192}, {}),
+    ("strip-2", "A", 38, "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 2, "i": 4096}, {}),
+    ("small-nt", "L", 9, "A.0.i,B.1.x,O.1.x,W.0.i,W.1.x,X.1.i", {"x": 128, "i": 512}, {}),
 ]
 
 
