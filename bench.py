@@ -262,6 +262,15 @@ def cpu_eval_sample(seconds: float, workloads, seed: int = 0, cap_s: float = 6.0
                       f"BLAS {blas}"}
 
 
+def arm_config(workloads) -> dict:
+    """The workload both arms measure (identical dicts: the driver compares them);
+    how each arm evaluates a candidate goes under "method"."""
+    from paper_2604_15272_b200 import population as P
+    n = sum(len(P.units(P.load_population(w))) for w in workloads)
+    return {"workload": "five-workload SIGMA population: " + ",".join(workloads), "candidates": n,
+            "data": "synthetic inputs of the BASELINE shapes (R, G@14336, A, Q, L)"}
+
+
 def reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -285,9 +294,9 @@ def reference_arm(args) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1000,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "five-workload SIGMA population (R,G,A,Q,L)",
-                                            "path": "symfuse interp (CPU, baseline/_ref) + oracle port for G@14336",
-                                            "sample": "uniformly random candidates per step (seeded by step)"},
+            "data": "synthetic", "config": arm_config(workloads),
+            "method": {"path": "symfuse interp (CPU, baseline/_ref) + oracle port for G@14336",
+                       "sample": "uniformly random candidates per step (seeded by step)"},
             "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": os.cpu_count(), "kind": kind,
                              "sample": sample, "candidates_timed": cands, "capped": capped},
             "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -614,8 +623,8 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16/f32 timing + ff check", "data": "synthetic",
-        "config": {"workload": "five-workload SIGMA population: " + ",".join(args.workloads),
-                   "candidates": n_total, "per_candidate": "FF check (on-device mismatch count) + CUDA-event timing of one rotation of input "
+        "config": arm_config(args.workloads),
+        "method": {"per_candidate": "FF check (on-device mismatch count) + CUDA-event timing of one rotation of input "
                                     f"sets; top {args.refine_top} per workload re-timed over 1000 launches",
                    "l2": "inputs rotated over sets totalling >= 3x L2 (cold L2 per launch)",
                    "compile_s_rank0": compile_s},

@@ -63,3 +63,15 @@ def test_reference_arm_cpu_sample_is_uniform_and_capped(ref):
     assert r["kind"] in ("reference", "reference+port")
     assert "uniformly at random" in r["sample"]
     assert r["value"] == r["candidates"] / r["seconds"]
+
+
+def test_both_bench_arms_name_the_same_config():
+    """bench.py's GPU arm and `--impl reference` print the same `config` dict (the
+    workload: population, size, data); run-dependent figures and each arm's way of
+    evaluating a candidate go under `method`."""
+    import bench
+    src = open(bench.__file__).read()
+    assert src.count('"config": arm_config(') == 2
+    c = bench.arm_config(["R", "G", "A", "Q", "L"])
+    assert c["candidates"] == 1421 and "R,G,A,Q,L" in c["workload"]
+    assert all(not isinstance(v, float) for v in c.values())
