@@ -72,3 +72,36 @@ def test_planner_summaries_are_deterministic():
     u = _unit("Q", "O.3.x,V.3.x", {"x": 128, "i": 1}, template=37)
     a, b = _src(u, _abi.BF16), _src(u, _abi.BF16)
     assert a == b
+
+
+def _res_usage(p):
+    import os
+    import re
+    import subprocess
+    import tempfile
+    fd, path = tempfile.mkstemp(suffix=".cubin")
+    try:
+        os.write(fd, p.cubin())
+        os.close(fd)
+        out = subprocess.run(["cuobjdump", "-res-usage", path], capture_output=True, text=True).stdout
+    finally:
+        os.unlink(path)
+    m = re.search(r"REG:(\d+) STACK:(\d+)", out)
+    return int(m.group(1)), int(m.group(2))
+
+
+def test_wide_gsplit_tail_does_not_spill():
+    """A 128-way gsplit reduction tail (A's split-KV loop, finite field) reads its
+    partials in batches: holding all 128 in registers spilled the whole kernel
+    (255 registers + 432 B of stack, one CTA per SM)."""
+    import shutil
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not on PATH")
+    u = _unit("A", "Kt.3.i,O.3.x,V.2.i,V.3.x", {"x": 2, "i": 8192}, template=38)
+    p = S.Plan(u.cand, _abi.FF, None, None)
+    try:
+        assert "GP=128" in p.info["summary"]
+        regs, stack = _res_usage(p)
+    finally:
+        p.close()
+    assert regs < 200 and stack == 0, (regs, stack)
