@@ -707,7 +707,8 @@ struct Gen {
       if (xcache_loop) loop_iters *= miss;
       t_item *= miss + 0.5 * (1.0 - miss);
     }
-    t_item += loop_iters * 0.6e-6;
+    static const double iter_s = getenv("SGM_ITER_NS") ? atof(getenv("SGM_ITER_NS")) * 1e-9 : 0.6e-6;  // A/B experiments
+    t_item += loop_iters * iter_s;
     return t_stream + (double)rounds * t_item + over;
   }
 
